@@ -1,0 +1,188 @@
+/*
+ * delta.h — C ABI of the B200-native DELTA decode-step attention stack
+ * (DELTA: Dynamic Layer-Aware Token Attention, arXiv 2510.09883).
+ *
+ * The library implements ONE step of decoding through the three-tier attention
+ * stack of PAPER.md §4 (lines 157-185): FULL layers attend to the whole paged KV
+ * cache; Delta (SELECT) layers attend to the whole cache, score every token by its
+ * maximum normalised attention weight over all query heads and pick the top-k
+ * salient units plus the sink and recency window; SPARSE layers attend only to the
+ * units chosen by the nearest Delta layer below them, at this step.
+ *
+ * Citations: "PAPER.md:L" = line L of the paper's LaTeX (§, Eq.); "R#" = the reading
+ * of an ambiguous passage listed in DESIGN.md §3.  Index base is 0 (R25).
+ *
+ * Conventions (all entry points):
+ *  - Every device pointer is CALLER-OWNED (e.g. torch tensors).  The library never
+ *    allocates device memory after delta_create and never frees caller memory.
+ *  - Hot-path calls (append / decode / select / step) are asynchronous on the given
+ *    stream and never synchronise the host; their return value is host-side argument
+ *    and call-order validation only.  Device-side faults (NaN/Inf in an output,
+ *    a stale plan under graph replay) set a STICKY device flag read by delta_get_error.
+ *  - One writer per handle (calls on one handle must be ordered by the caller).
+ *  - All calls may be captured into a CUDA graph (no host syncs, device-resident
+ *    sequence lengths, fixed grids).
+ *  - Sizes: m = num_q_heads, g = num_kv_heads, gs = m/g, d = head_dim, P = page_size.
+ */
+#ifndef DELTA_H
+#define DELTA_H
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct delta_ctx* delta_t;
+
+typedef enum {
+    DELTA_OK = 0,
+    DELTA_ERR_CONFIG = 1,   /* invalid shapes / schedule / budget (SPEC "configuration error") */
+    DELTA_ERR_USAGE = 2,    /* bad layer or batch, call-order violation, stale plan */
+    DELTA_ERR_NUMERIC = 3,  /* NaN/Inf produced on device (sticky, via delta_get_error) */
+    DELTA_ERR_CAPACITY = 4, /* append past max_seq_len / pool too small */
+    DELTA_ERR_CUDA = 5,     /* a CUDA runtime call failed (message in delta_last_error_message) */
+    DELTA_ERR_NCCL = 6      /* collective failure (sequence-sharded mode) */
+} delta_status;
+
+typedef enum { DELTA_BF16 = 0, DELTA_FP32 = 1 } delta_dtype;
+
+typedef enum { DELTA_ROLE_FULL = 0, DELTA_ROLE_SELECT = 1, DELTA_ROLE_SPARSE = 2 } delta_role;
+
+/* Problem statement of the method (PAPER.md:157-158 schedule, 168-171/185 budget and
+ * window, 180-181/196 paged layout). */
+typedef struct {
+    int32_t num_layers;        /* L */
+    int32_t num_q_heads;       /* m */
+    int32_t num_kv_heads;      /* g, g | m; head j reads group phi(j) = j / (m/g) (R15) */
+    int32_t head_dim;          /* d in {64, 128} */
+    int32_t max_batch;         /* sequences per call, >= 1 */
+    int32_t max_seq_len;       /* cache capacity per sequence, tokens */
+    int32_t page_size;         /* P; PAPER.md:196 uses 16.  Must be 16. */
+    int32_t num_phys_pages;    /* pages per layer in each pool; 0 -> max_batch*ceil(max_seq_len/P) */
+    int32_t num_full_prefix;   /* F: layers [0, F) are FULL */
+    int32_t num_select_layers; /* |Delta| */
+    const int32_t* select_layers; /* host array, strictly ascending, each >= F; every layer >= F
+                                     must have a Delta layer <= it */
+    int32_t budget_k;          /* k: salient TOKENS selected beyond sink and window (R1) */
+    int32_t n_sink;            /* S: first S tokens always kept (R2) */
+    int32_t n_window;          /* L: last L tokens (incl. this step's) always kept (R3) */
+    int32_t select_block;      /* 1 = token-level selection,
+                                  P = page-level; page mode needs P | k (R6) */
+    delta_dtype kv_dtype;      /* dtype of K/V pools, q, k_new, v_new.  Outputs are fp32. */
+    float softmax_scale;       /* 0 -> (float)(1/sqrt(d))  (Eq.4, R16) */
+    int32_t shard_world;       /* sequence sharding across GPUs; 1 = off (must be 1 in this build) */
+    int32_t shard_rank;
+    const void* nccl_id;       /* reserved for sequence sharding */
+} delta_config;
+
+/* Caller-owned device buffers.  Sizes from delta_query_sizes. */
+typedef struct {
+    void* k_pool;              /* [L][num_phys_pages][g][P][d] kv_dtype: one "head-page" of P*d
+                                  contiguous elements per (layer, page, kv head) */
+    void* v_pool;              /* same layout */
+    const int32_t* block_table;/* [max_batch][ceil(max_seq_len/P)] int32 physical page ids,
+                                  shared by all layers: token t of sequence b lives in page
+                                  block_table[b][t/P], slot t%P (PAPER.md:181 p(t)) */
+    void* workspace;           /* >= workspace_bytes, 256-byte aligned, zero-initialised
+                                  by delta_create */
+    size_t workspace_bytes;
+} delta_buffers;
+
+/* Byte sizes of one pool (K or V) and of the workspace for this config on the CURRENT
+ * device.  CONFIG error if the config is invalid. */
+delta_status delta_query_sizes(const delta_config* cfg, size_t* pool_bytes_each,
+                               size_t* workspace_bytes);
+
+/* Validate the config (shapes, schedule as in SPEC.md:378-386, budget), compute each
+ * layer's role and governing Delta layer, carve the workspace, build TMA descriptors.
+ * Sets every cache length to 0.  Synchronous (host + one memset). */
+delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, delta_t* out);
+
+/* Set cache lengths (tokens already stored, e.g. after an external prefill) of
+ * sequences [0, batch) for one layer (layer >= 0) or all layers (layer == -1).
+ * lens_host: host array [batch].  CAPACITY if a length exceeds max_seq_len.
+ * Resets host-side call-order tracking. */
+delta_status delta_set_seq_lens(delta_t h, int32_t layer, int32_t batch,
+                                const int32_t* lens_host, cudaStream_t stream);
+
+/* Eq.7 KV append for one layer: K <- [K; k_new], V <- [V; v_new].
+ * k_new, v_new: device [batch][ntok][g][d] kv_dtype.  Token i of sequence b goes to
+ * position n_b + i (n_b = current length); lengths grow by ntok.  Never evicts
+ * (PAPER.md:161).  CAPACITY error is detected on device (sticky) if n_b+ntok > max. */
+delta_status delta_append_kv(delta_t h, int32_t layer, int32_t batch, int32_t ntok,
+                             const void* k_new, const void* v_new, cudaStream_t stream);
+
+/* Decode attention of one layer for sequences [0, batch), dispatched on the layer's role:
+ *  FULL   : Eq.4 over all s cached tokens.
+ *  SELECT : Eq.4 over all s tokens (R11: the Delta layer's own output is full attention),
+ *           and records the logits needed by delta_select.
+ *  SPARSE : Eq.4 over tokens(rho) of the governing Delta layer's plan from THIS step,
+ *           softmax renormalised over rho (R10, R13).  USAGE error if
+ *           that plan is stale (host check) — under graph replay the device check sets
+ *           the sticky USAGE flag and writes NaN outputs.
+ * q: device [batch][m][d] kv_dtype.  out: device [batch][m][d] fp32.
+ * lse_out: optional device [batch][m] fp32 natural-log LSE of each head's logits over
+ * the attended set (NULL to skip). */
+delta_status delta_decode_layer(delta_t h, int32_t layer, int32_t batch, const void* q,
+                                float* out, float* lse_out, cudaStream_t stream);
+
+/* Fused Eq.7 append of ONE token (k_new, v_new: [batch][g][d]) + delta_decode_layer,
+ * in a single launch: the new row is written to the pool and used from the input
+ * directly.  Same semantics as delta_append_kv(ntok=1) followed by delta_decode_layer. */
+delta_status delta_append_decode_layer(delta_t h, int32_t layer, int32_t batch,
+                                       const void* k_new, const void* v_new, const void* q,
+                                       float* out, float* lse_out, cudaStream_t stream);
+
+/* Selection at a Delta layer (PAPER.md:163-171 token form, 180-185 page form), after
+ * that layer's decode in the same step.  Per sequence:
+ *   key_t = max_j (a_j(t) - LSE_j) in fp32 (log of s_t = max_j alpha_j(t), R7/R8);
+ *   page mode: S_u = sum_{t in u} exp(key_t) in ascending t (fp32);
+ *   rho = forced (sink, window units) U top-(k/block) candidates by (key desc, index asc)
+ *   (R1-R6, R9, R12); all units if the candidates fit the budget.
+ * The plan (ascending unit ids, count, stamp = s) is kept in the workspace for the
+ * sparse layers this Delta layer governs.
+ * keys_override: NULL, or device [batch][ceil(s/select_block)] fp32 unit keys to rank
+ *   instead of this layer's scores (test hook; ranking and plan are identical code).
+ * idx_out / count_out: optional device copies of the plan, [batch][plan_capacity] int32
+ *   (entries past count are -1) and [batch] int32. */
+delta_status delta_select(delta_t h, int32_t layer, int32_t batch, const float* keys_override,
+                          int32_t* idx_out, int32_t* count_out, cudaStream_t stream);
+
+/* One whole decode step of the stack: for every layer l in order, fused append of
+ * k_all[l] / v_all[l] and decode with q_all[l], plus selection after each Delta layer.
+ * q_all: [L][batch][m][d]; k_all, v_all: [L][batch][g][d] (kv_dtype); out_all:
+ * [L][batch][m][d] fp32; lse_all: optional [L][batch][m] fp32.  The launch sequence
+ * is captured once into a CUDA graph per (batch, pointers, stream) and replayed. */
+delta_status delta_decode_step(delta_t h, int32_t batch, const void* q_all, const void* k_all,
+                               const void* v_all, float* out_all, float* lse_all,
+                               cudaStream_t stream);
+
+/* delta_decode_step with HOST buffers (pinned recommended): copies the step's inputs
+ * host->device into workspace staging, runs the step, copies out_all device->host, all
+ * on `stream`.  Returns after enqueueing; synchronise the stream before reading out. */
+delta_status delta_decode_step_host(delta_t h, int32_t batch, const void* q_all_host,
+                                    const void* k_all_host, const void* v_all_host,
+                                    float* out_all_host, cudaStream_t stream);
+
+/* Synchronises `stream`, reads and clears the sticky device error flag.
+ * *sticky = DELTA_OK or the first device-side error recorded. The only syncing call. */
+delta_status delta_get_error(delta_t h, cudaStream_t stream, delta_status* sticky);
+
+delta_role   delta_layer_role(delta_t h, int32_t layer);        /* -1 cast if out of range */
+int32_t      delta_governing_layer(delta_t h, int32_t layer);  /* Delta layer of a SPARSE layer */
+int32_t      delta_plan_capacity(delta_t h);                   /* max |rho| in units */
+const char*  delta_last_error_message(delta_t h);              /* NULL handle: global message */
+const char*  delta_version(void);
+delta_status delta_destroy(delta_t h);
+
+/* Launch statistics for the benchmark contract: number of kernels this handle has
+ * enqueued since creation (graph replays count their kernels). */
+uint64_t     delta_kernels_launched(delta_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DELTA_H */

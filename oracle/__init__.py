@@ -131,11 +131,13 @@ class SeqKV:
         V = np.asarray(V, dtype=np.float32)
         s, g, d = K.shape
         n_pages = max(1, -(-s // P))
-        kp = np.zeros((n_pages, g, P, d), np.float32)
-        vp = np.zeros((n_pages, g, P, d), np.float32)
-        for t in range(s):
-            kp[t // P, :, t % P, :] = K[t]
-            vp[t // P, :, t % P, :] = V[t]
+        kp = np.zeros((n_pages * P, g, d), np.float32)
+        vp = np.zeros((n_pages * P, g, d), np.float32)
+        kp[:s] = K
+        vp[:s] = V
+        # [pages*P][g][d] -> [pages][g][P][d]
+        kp = kp.reshape(n_pages, P, g, d).transpose(0, 2, 1, 3)
+        vp = vp.reshape(n_pages, P, g, d).transpose(0, 2, 1, 3)
         return cls(kp, vp, np.arange(n_pages, dtype=np.int32), P)
 
     @property

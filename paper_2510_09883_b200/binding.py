@@ -1,0 +1,255 @@
+"""ctypes binding of ``libdelta.so`` (include/delta.h) — argument marshalling only.
+
+Every step of the decode path runs in the library's sm_100a kernels.  There is no CPU or
+PyTorch fallback: if the shared library is missing this module raises on load.
+PyTorch provides device memory, streams and process groups (plumbing).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from dataclasses import dataclass, field
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdelta.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "delta.h")
+
+DELTA_BF16, DELTA_FP32 = 0, 1
+ROLE_FULL, ROLE_SELECT, ROLE_SPARSE = 0, 1, 2
+STATUS = {0: "OK", 1: "CONFIG", 2: "USAGE", 3: "NUMERIC", 4: "CAPACITY", 5: "CUDA", 6: "NCCL"}
+
+
+class DeltaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"DELTA_ERR_{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [
+        ("num_layers", ctypes.c_int32), ("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32), ("max_batch", ctypes.c_int32), ("max_seq_len", ctypes.c_int32),
+        ("page_size", ctypes.c_int32), ("num_phys_pages", ctypes.c_int32), ("num_full_prefix", ctypes.c_int32),
+        ("num_select_layers", ctypes.c_int32), ("select_layers", ctypes.POINTER(ctypes.c_int32)),
+        ("budget_k", ctypes.c_int32), ("n_sink", ctypes.c_int32), ("n_window", ctypes.c_int32),
+        ("select_block", ctypes.c_int32), ("kv_dtype", ctypes.c_int), ("softmax_scale", ctypes.c_float),
+        ("shard_world", ctypes.c_int32), ("shard_rank", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
+    ]
+
+
+class _Buffers(ctypes.Structure):
+    _fields_ = [("k_pool", ctypes.c_void_p), ("v_pool", ctypes.c_void_p), ("block_table", ctypes.c_void_p),
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
+
+
+_lib = None
+
+
+def load_library() -> ctypes.CDLL:
+    """Load libdelta.so; raise if it is not built (no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build(); "
+                           "there is no CPU/PyTorch fallback for the DELTA decode path")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, st = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int
+    L.delta_query_sizes.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(ctypes.c_size_t),
+                                    ctypes.POINTER(ctypes.c_size_t)]
+    L.delta_query_sizes.restype = st
+    L.delta_create.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(_Buffers), ctypes.POINTER(vp)]
+    L.delta_create.restype = st
+    L.delta_set_seq_lens.argtypes = [vp, i32, i32, ctypes.POINTER(i32), vp]
+    L.delta_set_seq_lens.restype = st
+    L.delta_append_kv.argtypes = [vp, i32, i32, i32, vp, vp, vp]
+    L.delta_append_kv.restype = st
+    L.delta_decode_layer.argtypes = [vp, i32, i32, vp, vp, vp, vp]
+    L.delta_decode_layer.restype = st
+    L.delta_append_decode_layer.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp]
+    L.delta_append_decode_layer.restype = st
+    L.delta_select.argtypes = [vp, i32, i32, vp, vp, vp, vp]
+    L.delta_select.restype = st
+    L.delta_decode_step.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
+    L.delta_decode_step.restype = st
+    L.delta_decode_step_host.argtypes = [vp, i32, vp, vp, vp, vp, vp]
+    L.delta_decode_step_host.restype = st
+    L.delta_get_error.argtypes = [vp, vp, ctypes.POINTER(st)]
+    L.delta_get_error.restype = st
+    L.delta_layer_role.argtypes = [vp, i32]
+    L.delta_layer_role.restype = st
+    L.delta_governing_layer.argtypes = [vp, i32]
+    L.delta_governing_layer.restype = i32
+    L.delta_plan_capacity.argtypes = [vp]
+    L.delta_plan_capacity.restype = i32
+    L.delta_last_error_message.argtypes = [vp]
+    L.delta_last_error_message.restype = ctypes.c_char_p
+    L.delta_version.argtypes = []
+    L.delta_version.restype = ctypes.c_char_p
+    L.delta_destroy.argtypes = [vp]
+    L.delta_destroy.restype = st
+    L.delta_kernels_launched.argtypes = [vp]
+    L.delta_kernels_launched.restype = ctypes.c_uint64
+    _lib = L
+    return L
+
+
+def declared_functions() -> list[str]:
+    """Function names declared in include/delta.h (the boundary)."""
+    src = open(HEADER_PATH).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(delta_[a-z_0-9]+)\s*\(", src)))
+
+
+@dataclass
+class DeltaConfig:
+    """Problem statement of the method: schedule, budget, paged layout (include/delta.h)."""
+    num_layers: int
+    num_q_heads: int
+    num_kv_heads: int
+    head_dim: int
+    max_batch: int
+    max_seq_len: int
+    num_full_prefix: int
+    select_layers: list = field(default_factory=list)
+    budget_k: int = 2048
+    n_sink: int = 4
+    n_window: int = 32
+    select_block: int = 16
+    kv_dtype: int = DELTA_BF16
+    softmax_scale: float = 0.0
+    page_size: int = 16
+    num_phys_pages: int = 0
+    shard_world: int = 1
+    shard_rank: int = 0
+
+    def to_c(self):
+        arr = (ctypes.c_int32 * max(1, len(self.select_layers)))(*self.select_layers)
+        c = _Config(self.num_layers, self.num_q_heads, self.num_kv_heads, self.head_dim, self.max_batch,
+                    self.max_seq_len, self.page_size, self.num_phys_pages, self.num_full_prefix,
+                    len(self.select_layers), arr, self.budget_k, self.n_sink, self.n_window, self.select_block,
+                    self.kv_dtype, self.softmax_scale, self.shard_world, self.shard_rank, None)
+        return c, arr  # keep arr alive
+
+    @property
+    def max_pages(self) -> int:
+        return -(-self.max_seq_len // self.page_size)
+
+    @property
+    def phys_pages(self) -> int:
+        return self.num_phys_pages or self.max_batch * self.max_pages
+
+
+def _check(st: int, handle=None):
+    if st != 0:
+        msg = load_library().delta_last_error_message(handle)
+        raise DeltaError(st, msg.decode() if msg else "")
+
+
+def query_sizes(cfg: DeltaConfig) -> tuple[int, int]:
+    L = load_library()
+    c, _keep = cfg.to_c()
+    pb, wb = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(L.delta_query_sizes(ctypes.byref(c), ctypes.byref(pb), ctypes.byref(wb)))
+    return pb.value, wb.value
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class DeltaStack:
+    """One handle of the DELTA decode-attention stack over caller-owned torch buffers."""
+
+    def __init__(self, cfg: DeltaConfig, k_pool, v_pool, block_table, workspace):
+        self.cfg = cfg
+        self.lib = load_library()
+        self.k_pool, self.v_pool, self.block_table, self.workspace = k_pool, v_pool, block_table, workspace
+        c, self._keep = cfg.to_c()
+        b = _Buffers(k_pool.data_ptr(), v_pool.data_ptr(), block_table.data_ptr(), workspace.data_ptr(),
+                     workspace.numel() * workspace.element_size())
+        h = ctypes.c_void_p()
+        _check(self.lib.delta_create(ctypes.byref(c), ctypes.byref(b), ctypes.byref(h)))
+        self.h = h
+
+    @classmethod
+    def allocate(cls, cfg: DeltaConfig, block_table, device="cuda"):
+        """Allocate pools + workspace with torch (1024-byte aligned) and create the handle."""
+        import torch
+        pool_bytes, ws_bytes = query_sizes(cfg)
+        dt = torch.bfloat16 if cfg.kv_dtype == DELTA_BF16 else torch.float32
+        shape = (cfg.num_layers, cfg.phys_pages, cfg.num_kv_heads, cfg.page_size, cfg.head_dim)
+        k_pool = torch.zeros(shape, dtype=dt, device=device)
+        v_pool = torch.zeros(shape, dtype=dt, device=device)
+        assert k_pool.numel() * k_pool.element_size() == pool_bytes
+        ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=device)
+        bt = block_table.to(device=device, dtype=torch.int32).contiguous()
+        return cls(cfg, k_pool, v_pool, bt, ws)
+
+    # ------------------------------------------------------------------ calls
+    def set_seq_lens(self, lens, layer: int = -1, stream=None):
+        arr = (ctypes.c_int32 * len(lens))(*[int(x) for x in lens])
+        _check(self.lib.delta_set_seq_lens(self.h, layer, len(lens), arr, _stream(stream)), self.h)
+
+    def append_kv(self, layer: int, k_new, v_new, stream=None):
+        batch, ntok = k_new.shape[0], k_new.shape[1]
+        _check(self.lib.delta_append_kv(self.h, layer, batch, ntok, k_new.data_ptr(), v_new.data_ptr(),
+                                        _stream(stream)), self.h)
+
+    def decode_layer(self, layer: int, q, out, lse=None, stream=None):
+        _check(self.lib.delta_decode_layer(self.h, layer, q.shape[0], q.data_ptr(), out.data_ptr(), _ptr(lse),
+                                           _stream(stream)), self.h)
+
+    def append_decode_layer(self, layer: int, k_new, v_new, q, out, lse=None, stream=None):
+        _check(self.lib.delta_append_decode_layer(self.h, layer, q.shape[0], k_new.data_ptr(), v_new.data_ptr(),
+                                                  q.data_ptr(), out.data_ptr(), _ptr(lse), _stream(stream)), self.h)
+
+    def select(self, layer: int, batch: int, keys_override=None, idx_out=None, count_out=None, stream=None):
+        _check(self.lib.delta_select(self.h, layer, batch, _ptr(keys_override), _ptr(idx_out), _ptr(count_out),
+                                     _stream(stream)), self.h)
+
+    def decode_step(self, q_all, k_all, v_all, out_all, lse_all=None, stream=None):
+        _check(self.lib.delta_decode_step(self.h, q_all.shape[1], q_all.data_ptr(), k_all.data_ptr(),
+                                          v_all.data_ptr(), out_all.data_ptr(), _ptr(lse_all), _stream(stream)),
+               self.h)
+
+    def decode_step_host(self, q_host, k_host, v_host, out_host, stream=None):
+        _check(self.lib.delta_decode_step_host(self.h, q_host.shape[1], q_host.data_ptr(), k_host.data_ptr(),
+                                               v_host.data_ptr(), out_host.data_ptr(), _stream(stream)), self.h)
+
+    def get_error(self, stream=None) -> int:
+        v = ctypes.c_int()
+        _check(self.lib.delta_get_error(self.h, _stream(stream), ctypes.byref(v)), self.h)
+        return v.value
+
+    def role(self, layer: int) -> int:
+        return self.lib.delta_layer_role(self.h, layer)
+
+    def governing(self, layer: int) -> int:
+        return self.lib.delta_governing_layer(self.h, layer)
+
+    @property
+    def plan_capacity(self) -> int:
+        return self.lib.delta_plan_capacity(self.h)
+
+    @property
+    def kernels_launched(self) -> int:
+        return int(self.lib.delta_kernels_launched(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.delta_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,57 @@
+// append.cu — Eq.7 KV append: K <- [K; k_new], V <- [V; v_new] for one
+// layer; token i of sequence b goes to position n_b + i = page block_table[b][pos/P],
+// slot pos % P, then seq_len[b] grows by ntok.  The cache is append-only.
+// One CTA per sequence, 16-byte vector copies.
+#include "combine.cuh"
+
+namespace delta {
+namespace {
+
+__global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
+    const int b = blockIdx.x;
+    pdl_wait();
+    const int n = p.seq_len[p.layer * p.max_batch + b];
+    if (n + p.ntok > p.max_seq) {
+        if (threadIdx.x == 0) set_err(p.err, kDevCapacity);
+        return;
+    }
+    const int row_bytes = p.d * p.elem_bytes;        // one head row
+    const int chunks = row_bytes / 16;               // 16-byte chunks per row
+    const int total = p.ntok * p.g * chunks;
+    const uint8_t* ks = reinterpret_cast<const uint8_t*>(p.k_new) + (size_t)b * p.ntok * p.g * row_bytes;
+    const uint8_t* vs = reinterpret_cast<const uint8_t*>(p.v_new) + (size_t)b * p.ntok * p.g * row_bytes;
+    const int32_t* bt = p.block_table + (size_t)b * p.bt_stride;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+        const int c = i % chunks;
+        const int hh = (i / chunks) % p.g;
+        const int tok = i / (chunks * p.g);
+        const int t = n + tok;
+        const size_t row = (((size_t)p.layer * p.num_phys + bt[t / kPage]) * p.g + hh) * kPage + (t % kPage);
+        const size_t src_off = ((size_t)tok * p.g + hh) * row_bytes + (size_t)c * 16;
+        const size_t dst_off = row * row_bytes + (size_t)c * 16;
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.k_pool) + dst_off) =
+            *reinterpret_cast<const uint4*>(ks + src_off);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.v_pool) + dst_off) =
+            *reinterpret_cast<const uint4*>(vs + src_off);
+    }
+    __syncthreads();
+    pdl_launch_dependents();
+    if (threadIdx.x == 0) p.seq_len[p.layer * p.max_batch + b] = n + p.ntok;
+}
+
+}  // namespace
+
+cudaError_t launch_append(const AppendParams& p, cudaStream_t st, bool pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.batch);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, append_kernel, p);
+}
+
+}  // namespace delta

@@ -1,0 +1,597 @@
+// delta_api.cu — host runtime behind include/delta.h: configuration validation and the
+// three-tier schedule, workspace carving,
+// TMA descriptors, launch sizing, call-order (plan freshness) tracking, and the CUDA-graph
+// step driver.  All device work is in the kernels; this file only marshals and launches.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/delta.h"
+#include "internal.h"
+
+using namespace delta;
+
+namespace {
+
+thread_local std::string g_msg;
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Layout {
+    size_t seq_len, err, cnt_head, cnt_seq, cnt_sel, part_o, part_lse, logits, lse_buf, keys,
+        plan_idx, plan_count, plan_stamp, stage_q, stage_k, stage_v, stage_out, total;
+    int rows_max, max_units, plan_cap, n_delta, max_pages;
+};
+
+int num_sms_current() {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+    }
+    cudaGetLastError();  // no device (CPU-only host) -> keep the B200 default
+    return sms > 0 ? sms : 148;
+}
+
+int nsplit_full(int batch, int g, int sms, int max_pages) {
+    int n = (2 * sms) / std::max(1, batch * g);
+    n = std::max(1, std::min(n, kMaxSplit));
+    return std::min(n, std::max(1, max_pages));
+}
+
+int plan_tiles(const delta_config& c, int plan_cap) {
+    return c.select_block == 1 ? (plan_cap + 15) / 16 : plan_cap;
+}
+
+int nsplit_sparse(const delta_config& c, int batch, int sms, int max_pages, int plan_cap) {
+    const int full = nsplit_full(batch, c.num_kv_heads, sms, max_pages);
+    const int by_tiles = std::max(1, (plan_tiles(c, plan_cap) + 3) / 4);  // >= one 4-tile stage each
+    return std::max(1, std::min(full, by_tiles));
+}
+
+int elem_bytes(const delta_config& c) { return c.kv_dtype == DELTA_BF16 ? 2 : 4; }
+
+// Validation (returns empty string if OK), following SPEC.md:378-386.
+std::string validate(const delta_config& c, std::vector<int>& role, std::vector<int>& gov) {
+    char buf[256];
+    if (c.num_layers < 1) return "num_layers must be >= 1";
+    if (c.num_q_heads < 1 || c.num_kv_heads < 1 || c.num_q_heads % c.num_kv_heads != 0)
+        return "num_kv_heads must divide num_q_heads";
+    if (c.num_q_heads / c.num_kv_heads > kMaxGs) return "num_q_heads / num_kv_heads must be <= 16";
+    if (c.num_q_heads > 256) return "num_q_heads must be <= 256";
+    if (c.head_dim != 64 && c.head_dim != 128) return "head_dim must be 64 or 128";
+    if (c.max_batch < 1 || c.max_seq_len < 1) return "max_batch and max_seq_len must be >= 1";
+    if (c.page_size != kPage) return "page_size must be 16 (PAPER.md:196)";
+    if (c.kv_dtype != DELTA_BF16 && c.kv_dtype != DELTA_FP32) return "kv_dtype must be BF16 or FP32";
+    if (c.num_full_prefix < 0 || c.num_full_prefix > c.num_layers) return "num_full_prefix out of range";
+    if (c.num_select_layers < 0 || (c.num_select_layers > 0 && !c.select_layers))
+        return "select_layers missing";
+    if (c.budget_k < 0 || c.n_sink < 0 || c.n_window < 0) return "budget_k, n_sink, n_window must be >= 0";
+    if (c.select_block != 1 && c.select_block != c.page_size) return "select_block must be 1 or page_size";
+    if (c.select_block == c.page_size && c.budget_k % c.page_size != 0)
+        return "page-level selection needs budget_k % page_size == 0 (R6)";
+    if (c.shard_world != 1 || c.shard_rank != 0) return "sequence sharding (shard_world > 1) is not built in this library version";
+    if (c.softmax_scale < 0.f || !std::isfinite(c.softmax_scale)) return "softmax_scale must be finite and >= 0";
+    role.assign(c.num_layers, kRoleSparse);
+    gov.assign(c.num_layers, -1);
+    for (int i = 0; i < c.num_select_layers; ++i) {
+        const int l = c.select_layers[i];
+        if (l < c.num_full_prefix || l >= c.num_layers) {
+            snprintf(buf, sizeof buf, "Delta layer %d inside the full prefix or out of range", l);
+            return buf;
+        }
+        if (i > 0 && l <= c.select_layers[i - 1]) return "select_layers must be strictly ascending";
+    }
+    int current = -1, next = 0;
+    for (int l = 0; l < c.num_layers; ++l) {
+        if (l < c.num_full_prefix) {
+            role[l] = kRoleFull; gov[l] = l;
+        } else if (next < c.num_select_layers && c.select_layers[next] == l) {
+            role[l] = kRoleSelect; gov[l] = l; current = l; ++next;
+        } else {
+            if (current < 0) {
+                snprintf(buf, sizeof buf, "layer %d has no Delta layer at or below it (SPEC.md:382)", l);
+                return buf;
+            }
+            role[l] = kRoleSparse; gov[l] = current;
+        }
+    }
+    return "";
+}
+
+Layout layout(const delta_config& c, int sms) {
+    Layout L = {};
+    const int m = c.num_q_heads, g = c.num_kv_heads, D = c.head_dim;
+    const size_t e = elem_bytes(c);
+    L.max_pages = (c.max_seq_len + kPage - 1) / kPage;
+    L.max_units = (c.max_seq_len + c.select_block - 1) / c.select_block;
+    L.n_delta = c.num_select_layers;
+    {   // plan capacity in units: salient k/block + max sink units + max window units
+        const int blk = c.select_block;
+        const int k_units = c.budget_k / blk;
+        const int sink_units = c.n_sink > 0 ? (c.n_sink + blk - 1) / blk : 0;
+        const int win_units = c.n_window > 0 ? (blk == 1 ? c.n_window : (c.n_window - 1) / blk + 2) : 0;
+        L.plan_cap = std::max(1, std::min(L.max_units, k_units + sink_units + win_units));
+    }
+    int rows = 0;
+    for (int b = 1; b <= c.max_batch; ++b)
+        rows = std::max(rows, b * std::max(nsplit_full(b, g, sms, L.max_pages),
+                                           nsplit_sparse(c, b, sms, L.max_pages, L.plan_cap)));
+    L.rows_max = rows;
+    const bool has_sel = c.num_select_layers > 0;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + std::max<size_t>(bytes, 1)); return o; };
+    L.seq_len = take((size_t)c.num_layers * c.max_batch * 4);
+    L.err = take(16);
+    L.cnt_head = take((size_t)c.num_layers * c.max_batch * g * 4);
+    L.cnt_seq = take((size_t)c.num_layers * c.max_batch * 4);
+    L.cnt_sel = take((size_t)c.num_layers * c.max_batch * 4);
+    L.part_o = take((size_t)rows * m * D * 4);
+    L.part_lse = take((size_t)rows * m * 4);
+    L.logits = take(has_sel ? (size_t)c.max_batch * c.max_seq_len * m * 4 : 0);
+    L.lse_buf = take((size_t)c.max_batch * m * 4);
+    L.keys = take(has_sel ? (size_t)c.max_batch * L.max_units * 4 : 0);
+    const int nd = std::max(1, L.n_delta);
+    L.plan_idx = take((size_t)nd * c.max_batch * L.plan_cap * 4);
+    L.plan_count = take((size_t)nd * c.max_batch * 4);
+    L.plan_stamp = take((size_t)nd * c.max_batch * 4);
+    L.stage_q = take((size_t)c.num_layers * c.max_batch * m * D * e);
+    L.stage_k = take((size_t)c.num_layers * c.max_batch * g * D * e);
+    L.stage_v = take((size_t)c.num_layers * c.max_batch * g * D * e);
+    L.stage_out = take((size_t)c.num_layers * c.max_batch * m * D * 4);
+    L.total = off;
+    return L;
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+}  // namespace
+
+struct delta_ctx {
+    delta_config cfg;
+    std::vector<int32_t> select_layers;
+    std::vector<int> role, gov, slot;  // slot: Delta layer -> plan index
+    Layout L;
+    int sms = 148, gs = 1;
+    uint8_t* ws = nullptr;
+    void* k_pool = nullptr;
+    void* v_pool = nullptr;
+    const int32_t* block_table = nullptr;
+    CUtensorMap tm_k, tm_v;
+    bool use_tc = false;
+    float scale = 0.f;
+    std::vector<long long> step, dec_step, sel_step;
+    // graph cache for delta_decode_step
+    cudaGraphExec_t gexec = nullptr;
+    const void* gkey[7] = {};
+    int gbatch = -1;
+    uint64_t graph_kernels = 0;
+    uint64_t launches = 0;
+    bool pdl = true;
+    std::string msg;
+
+    template <typename T>
+    T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
+};
+
+namespace {
+
+delta_status fail(delta_ctx* h, delta_status st, const std::string& m) {
+    if (h) h->msg = m; else g_msg = m;
+    return st;
+}
+
+delta_status cuda_fail(delta_ctx* h, cudaError_t e, const char* what) {
+    return fail(h, DELTA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+AttnParams attn_params(delta_ctx* h, int layer, int batch) {
+    const delta_config& c = h->cfg;
+    AttnParams p = {};
+    p.m = c.num_q_heads; p.g = c.num_kv_heads; p.gs = h->gs; p.d = c.head_dim;
+    p.layer = layer; p.batch = batch; p.role = h->role[layer];
+    p.num_phys = c.num_phys_pages; p.bt_stride = h->L.max_pages;
+    p.max_batch = c.max_batch; p.max_seq = c.max_seq_len;
+    p.sel_block = c.select_block; p.plan_cap = h->L.plan_cap;
+    p.scale = h->scale; p.scale_log2 = (float)((double)h->scale * 1.4426950408889634);
+    p.k_pool = h->k_pool; p.v_pool = h->v_pool; p.block_table = h->block_table;
+    p.seq_len = h->at<int32_t>(h->L.seq_len);
+    p.part_o = h->at<float>(h->L.part_o); p.part_lse = h->at<float>(h->L.part_lse);
+    p.cnt_head = h->at<int32_t>(h->L.cnt_head) + (size_t)layer * c.max_batch * c.num_kv_heads;
+    p.cnt_seq = h->at<int32_t>(h->L.cnt_seq) + (size_t)layer * c.max_batch;
+    p.logits = h->at<float>(h->L.logits); p.lse_buf = h->at<float>(h->L.lse_buf);
+    p.err = h->at<int32_t>(h->L.err);
+    if (p.role == kRoleSparse) {
+        const int sl = h->slot[h->gov[layer]];
+        p.plan_idx = h->at<int32_t>(h->L.plan_idx) + (size_t)sl * c.max_batch * h->L.plan_cap;
+        p.plan_count = h->at<int32_t>(h->L.plan_count) + (size_t)sl * c.max_batch;
+        p.plan_stamp = h->at<int32_t>(h->L.plan_stamp) + (size_t)sl * c.max_batch;
+        p.nsplit = nsplit_sparse(c, batch, h->sms, h->L.max_pages, h->L.plan_cap);
+    } else {
+        p.nsplit = nsplit_full(batch, c.num_kv_heads, h->sms, h->L.max_pages);
+    }
+    return p;
+}
+
+delta_status check_layer_batch(delta_ctx* h, int layer, int batch) {
+    if (!h) return fail(nullptr, DELTA_ERR_USAGE, "null handle");
+    if (layer < 0 || layer >= h->cfg.num_layers) return fail(h, DELTA_ERR_USAGE, "layer out of range");
+    if (batch < 1 || batch > h->cfg.max_batch) return fail(h, DELTA_ERR_USAGE, "batch out of range");
+    return DELTA_OK;
+}
+
+// host-side plan freshness: a SPARSE layer may only run after its governing
+// Delta layer selected at THIS step (R13).
+delta_status check_sparse_fresh(delta_ctx* h, int layer, bool appending) {
+    if (h->role[layer] != kRoleSparse) return DELTA_OK;
+    const int d = h->gov[layer];
+    const long long my_step = h->step[layer] + (appending ? 1 : 0);
+    if (h->sel_step[h->slot[d]] != h->step[d] || my_step != h->step[d])
+        return fail(h, DELTA_ERR_USAGE,
+                    "stale plan: layer " + std::to_string(layer) + " needs delta_select on Delta layer " +
+                        std::to_string(d) + " at this step (PAPER.md:160-161)");
+    return DELTA_OK;
+}
+
+delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new, const void* v_new,
+                           const void* q, float* out, float* lse_out, cudaStream_t st) {
+    AttnParams p = attn_params(h, layer, batch);
+    p.q = q; p.out = out; p.lse_out = lse_out;
+    p.fuse_append = (k_new != nullptr);
+    p.k_new = k_new; p.v_new = v_new;
+    cudaError_t e = h->use_tc ? launch_attn_tc(p, &h->tm_k, &h->tm_v, st, h->pdl)
+                              : launch_attn_simt(p, h->cfg.kv_dtype == DELTA_BF16, st, h->pdl);
+    if (e != cudaSuccess) return cuda_fail(h, e, "decode launch");
+    ++h->launches;
+    return DELTA_OK;
+}
+
+delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_override, int32_t* idx_out,
+                        int32_t* count_out, cudaStream_t st) {
+    const delta_config& c = h->cfg;
+    SelectParams p = {};
+    const int sl = h->slot[layer];
+    p.m = c.num_q_heads; p.layer = layer; p.batch = batch;
+    p.nchunk = std::max(1, std::min((h->L.max_units + 15) / 16, (2 * h->sms + batch - 1) / batch));
+    p.sel_block = c.select_block; p.n_sink = c.n_sink; p.n_window = c.n_window;
+    p.k_units = c.budget_k / c.select_block;
+    p.max_batch = c.max_batch; p.max_seq = c.max_seq_len; p.max_units = h->L.max_units; p.plan_cap = h->L.plan_cap;
+    p.seq_len = h->at<int32_t>(h->L.seq_len);
+    p.logits = h->at<float>(h->L.logits); p.lse_buf = h->at<float>(h->L.lse_buf);
+    p.keys_override = keys_override; p.keys = h->at<float>(h->L.keys);
+    p.plan_idx = h->at<int32_t>(h->L.plan_idx) + (size_t)sl * c.max_batch * h->L.plan_cap;
+    p.plan_count = h->at<int32_t>(h->L.plan_count) + (size_t)sl * c.max_batch;
+    p.plan_stamp = h->at<int32_t>(h->L.plan_stamp) + (size_t)sl * c.max_batch;
+    p.idx_out = idx_out; p.count_out = count_out;
+    p.cnt = h->at<int32_t>(h->L.cnt_sel) + (size_t)layer * c.max_batch;
+    p.err = h->at<int32_t>(h->L.err);
+    cudaError_t e = launch_select(p, st, h->pdl);
+    if (e != cudaSuccess) return cuda_fail(h, e, "select launch");
+    ++h->launches;
+    return DELTA_OK;
+}
+
+// enqueue one whole step (fused append + decode per layer, select after Delta layers)
+delta_status enqueue_step(delta_ctx* h, int batch, const void* q_all, const void* k_all, const void* v_all,
+                          float* out_all, float* lse_all, cudaStream_t st) {
+    const delta_config& c = h->cfg;
+    const size_t e = elem_bytes(c);
+    const size_t q_l = (size_t)batch * c.num_q_heads * c.head_dim;
+    const size_t kv_l = (size_t)batch * c.num_kv_heads * c.head_dim;
+    for (int l = 0; l < c.num_layers; ++l) {
+        const uint8_t* q = static_cast<const uint8_t*>(q_all) + l * q_l * e;
+        const uint8_t* k = static_cast<const uint8_t*>(k_all) + l * kv_l * e;
+        const uint8_t* v = static_cast<const uint8_t*>(v_all) + l * kv_l * e;
+        delta_status s = launch_decode(h, l, batch, k, v, q, out_all + l * q_l,
+                                       lse_all ? lse_all + (size_t)l * batch * c.num_q_heads : nullptr, st);
+        if (s != DELTA_OK) return s;
+        if (h->role[l] == kRoleSelect) {
+            s = launch_sel(h, l, batch, nullptr, nullptr, nullptr, st);
+            if (s != DELTA_OK) return s;
+        }
+    }
+    return DELTA_OK;
+}
+
+void mark_step_done(delta_ctx* h) {
+    for (int l = 0; l < h->cfg.num_layers; ++l) {
+        h->step[l] += 1;
+        h->dec_step[l] = h->step[l];
+        if (h->role[l] == kRoleSelect) h->sel_step[h->slot[l]] = h->step[l];
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* delta_version(void) { return "delta-b200 0.1 (sm_100a)"; }
+
+delta_status delta_query_sizes(const delta_config* cfg, size_t* pool_bytes_each, size_t* workspace_bytes) {
+    if (!cfg) return fail(nullptr, DELTA_ERR_CONFIG, "null config");
+    std::vector<int> role, gov;
+    std::string err = validate(*cfg, role, gov);
+    if (!err.empty()) return fail(nullptr, DELTA_ERR_CONFIG, err);
+    delta_config c = *cfg;
+    const int max_pages = (c.max_seq_len + kPage - 1) / kPage;
+    const long long phys = c.num_phys_pages > 0 ? c.num_phys_pages : (long long)c.max_batch * max_pages;
+    if (pool_bytes_each)
+        *pool_bytes_each = (size_t)c.num_layers * phys * c.num_kv_heads * kPage * c.head_dim * elem_bytes(c);
+    if (workspace_bytes) *workspace_bytes = layout(c, num_sms_current()).total;
+    return DELTA_OK;
+}
+
+delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, delta_t* out) {
+    if (!cfg || !bufs || !out) return fail(nullptr, DELTA_ERR_USAGE, "null argument");
+    *out = nullptr;
+    std::vector<int> role, gov;
+    std::string err = validate(*cfg, role, gov);
+    if (!err.empty()) return fail(nullptr, DELTA_ERR_CONFIG, err);
+    delta_ctx* h = new delta_ctx();
+    h->cfg = *cfg;
+    h->select_layers.assign(cfg->select_layers, cfg->select_layers + cfg->num_select_layers);
+    h->cfg.select_layers = h->select_layers.data();
+    const int max_pages = (cfg->max_seq_len + kPage - 1) / kPage;
+    if (h->cfg.num_phys_pages <= 0) h->cfg.num_phys_pages = cfg->max_batch * max_pages;
+    h->role = role; h->gov = gov;
+    h->slot.assign(cfg->num_layers, -1);
+    for (int i = 0; i < cfg->num_select_layers; ++i) h->slot[cfg->select_layers[i]] = i;
+    h->sms = num_sms_current();
+    h->gs = cfg->num_q_heads / cfg->num_kv_heads;
+    h->L = layout(h->cfg, h->sms);
+    h->scale = cfg->softmax_scale > 0.f ? cfg->softmax_scale : (float)(1.0 / std::sqrt((double)cfg->head_dim));
+    if (!bufs->k_pool || !bufs->v_pool || !bufs->block_table || !bufs->workspace) {
+        delete h;
+        return fail(nullptr, DELTA_ERR_USAGE, "null buffer");
+    }
+    if (bufs->workspace_bytes < h->L.total) {
+        delete h;
+        return fail(nullptr, DELTA_ERR_CAPACITY, "workspace too small: need " + std::to_string(h->L.total));
+    }
+    if (reinterpret_cast<uintptr_t>(bufs->workspace) % kAlign || reinterpret_cast<uintptr_t>(bufs->k_pool) % 1024 ||
+        reinterpret_cast<uintptr_t>(bufs->v_pool) % 1024) {
+        delete h;
+        return fail(nullptr, DELTA_ERR_USAGE, "workspace must be 256-byte and pools 1024-byte aligned");
+    }
+    h->ws = static_cast<uint8_t*>(bufs->workspace);
+    h->k_pool = bufs->k_pool; h->v_pool = bufs->v_pool; h->block_table = bufs->block_table;
+    h->use_tc = (cfg->kv_dtype == DELTA_BF16);
+    if (h->use_tc) {
+        const unsigned long long rows =
+            (unsigned long long)cfg->num_layers * h->cfg.num_phys_pages * cfg->num_kv_heads * kPage;
+        if (rows >= (1ull << 31)) {
+            delete h;
+            return fail(nullptr, DELTA_ERR_CONFIG, "pool too large for 32-bit TMA row coordinates");
+        }
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || !fn || q != cudaDriverEntryPointSuccess) {
+            delete h;
+            return fail(nullptr, DELTA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        }
+        auto encode = reinterpret_cast<PFN_encodeTiled>(fn);
+        const cuuint64_t dims[2] = {(cuuint64_t)cfg->head_dim, (cuuint64_t)rows};
+        const cuuint64_t strides[1] = {(cuuint64_t)cfg->head_dim * 2};
+        const cuuint32_t box[2] = {64, (cuuint32_t)kPage};
+        const cuuint32_t estr[2] = {1, 1};
+        for (int i = 0; i < 2; ++i) {
+            CUresult r = encode(i == 0 ? &h->tm_k : &h->tm_v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                i == 0 ? bufs->k_pool : bufs->v_pool, dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) {
+                delete h;
+                return fail(nullptr, DELTA_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+            }
+        }
+    }
+    cudaError_t e = cudaMemset(h->ws, 0, h->L.total);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        std::string m = std::string("workspace init: ") + cudaGetErrorString(e);
+        delete h;
+        return fail(nullptr, DELTA_ERR_CUDA, m);
+    }
+    h->step.assign(cfg->num_layers, 0);
+    h->dec_step.assign(cfg->num_layers, -1);
+    h->sel_step.assign(std::max(1, cfg->num_select_layers), -1);
+    *out = h;
+    return DELTA_OK;
+}
+
+delta_status delta_destroy(delta_t h) {
+    if (!h) return DELTA_ERR_USAGE;
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    delete h;
+    return DELTA_OK;
+}
+
+delta_status delta_set_seq_lens(delta_t h, int32_t layer, int32_t batch, const int32_t* lens_host,
+                                cudaStream_t stream) {
+    if (!h) return fail(nullptr, DELTA_ERR_USAGE, "null handle");
+    if (batch < 1 || batch > h->cfg.max_batch || !lens_host) return fail(h, DELTA_ERR_USAGE, "bad batch/lens");
+    if (layer < -1 || layer >= h->cfg.num_layers) return fail(h, DELTA_ERR_USAGE, "layer out of range");
+    for (int b = 0; b < batch; ++b)
+        if (lens_host[b] < 0 || lens_host[b] > h->cfg.max_seq_len)
+            return fail(h, DELTA_ERR_CAPACITY, "length exceeds max_seq_len");
+    int32_t* sl = h->at<int32_t>(h->L.seq_len);
+    const int l0 = layer < 0 ? 0 : layer, l1 = layer < 0 ? h->cfg.num_layers : layer + 1;
+    for (int l = l0; l < l1; ++l) {
+        cudaError_t e = cudaMemcpyAsync(sl + (size_t)l * h->cfg.max_batch, lens_host, sizeof(int32_t) * batch,
+                                        cudaMemcpyHostToDevice, stream);
+        if (e != cudaSuccess) return cuda_fail(h, e, "set_seq_lens");
+    }
+    cudaError_t e = cudaStreamSynchronize(stream);  // lens_host may be freed by the caller after return
+    if (e != cudaSuccess) return cuda_fail(h, e, "set_seq_lens");
+    std::fill(h->step.begin(), h->step.end(), 0);
+    std::fill(h->dec_step.begin(), h->dec_step.end(), -1);
+    std::fill(h->sel_step.begin(), h->sel_step.end(), -1);
+    return DELTA_OK;
+}
+
+delta_status delta_append_kv(delta_t h, int32_t layer, int32_t batch, int32_t ntok, const void* k_new,
+                             const void* v_new, cudaStream_t stream) {
+    delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    if (ntok < 1 || !k_new || !v_new) return fail(h, DELTA_ERR_USAGE, "bad ntok or null k_new/v_new");
+    AppendParams p = {};
+    p.g = h->cfg.num_kv_heads; p.d = h->cfg.head_dim; p.layer = layer; p.batch = batch; p.ntok = ntok;
+    p.num_phys = h->cfg.num_phys_pages; p.bt_stride = h->L.max_pages; p.max_batch = h->cfg.max_batch;
+    p.max_seq = h->cfg.max_seq_len; p.elem_bytes = elem_bytes(h->cfg);
+    p.k_new = k_new; p.v_new = v_new; p.k_pool = h->k_pool; p.v_pool = h->v_pool;
+    p.block_table = h->block_table; p.seq_len = h->at<int32_t>(h->L.seq_len); p.err = h->at<int32_t>(h->L.err);
+    cudaError_t e = launch_append(p, stream, h->pdl);
+    if (e != cudaSuccess) return cuda_fail(h, e, "append launch");
+    ++h->launches;
+    h->step[layer] += 1;
+    return DELTA_OK;
+}
+
+delta_status delta_decode_layer(delta_t h, int32_t layer, int32_t batch, const void* q, float* out,
+                                float* lse_out, cudaStream_t stream) {
+    delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    if (!q || !out) return fail(h, DELTA_ERR_USAGE, "null q/out");
+    s = check_sparse_fresh(h, layer, false);
+    if (s != DELTA_OK) return s;
+    s = launch_decode(h, layer, batch, nullptr, nullptr, q, out, lse_out, stream);
+    if (s == DELTA_OK) h->dec_step[layer] = h->step[layer];
+    return s;
+}
+
+delta_status delta_append_decode_layer(delta_t h, int32_t layer, int32_t batch, const void* k_new,
+                                       const void* v_new, const void* q, float* out, float* lse_out,
+                                       cudaStream_t stream) {
+    delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    if (!q || !out || !k_new || !v_new) return fail(h, DELTA_ERR_USAGE, "null pointer");
+    s = check_sparse_fresh(h, layer, true);
+    if (s != DELTA_OK) return s;
+    s = launch_decode(h, layer, batch, k_new, v_new, q, out, lse_out, stream);
+    if (s == DELTA_OK) {
+        h->step[layer] += 1;
+        h->dec_step[layer] = h->step[layer];
+    }
+    return s;
+}
+
+delta_status delta_select(delta_t h, int32_t layer, int32_t batch, const float* keys_override, int32_t* idx_out,
+                          int32_t* count_out, cudaStream_t stream) {
+    delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    if (h->role[layer] != kRoleSelect) return fail(h, DELTA_ERR_USAGE, "delta_select on a non-Delta layer");
+    if (!keys_override && h->dec_step[layer] != h->step[layer])
+        return fail(h, DELTA_ERR_USAGE, "delta_select needs this layer's decode at the current step");
+    s = launch_sel(h, layer, batch, keys_override, idx_out, count_out, stream);
+    if (s == DELTA_OK) h->sel_step[h->slot[layer]] = h->step[layer];
+    return s;
+}
+
+delta_status delta_decode_step(delta_t h, int32_t batch, const void* q_all, const void* k_all, const void* v_all,
+                               float* out_all, float* lse_all, cudaStream_t stream) {
+    if (!h) return fail(nullptr, DELTA_ERR_USAGE, "null handle");
+    if (batch < 1 || batch > h->cfg.max_batch) return fail(h, DELTA_ERR_USAGE, "batch out of range");
+    if (!q_all || !k_all || !v_all || !out_all) return fail(h, DELTA_ERR_USAGE, "null pointer");
+    const bool legacy = (stream == 0 || stream == cudaStreamLegacy || stream == cudaStreamPerThread);
+    if (legacy) {  // default streams cannot be captured: run eagerly
+        delta_status s = enqueue_step(h, batch, q_all, k_all, v_all, out_all, lse_all, stream);
+        if (s == DELTA_OK) mark_step_done(h);
+        return s;
+    }
+    const void* key[7] = {q_all, k_all, v_all, out_all, lse_all, (const void*)stream, nullptr};
+    bool hit = h->gexec && h->gbatch == batch && std::memcmp(key, h->gkey, sizeof key) == 0;
+    if (!hit) {
+        if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+        for (int attempt = 0; attempt < 2 && !h->gexec; ++attempt) {
+            const uint64_t before = h->launches;
+            cudaError_t e = cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal);
+            if (e != cudaSuccess) return cuda_fail(h, e, "graph capture begin");
+            delta_status s = enqueue_step(h, batch, q_all, k_all, v_all, out_all, lse_all, stream);
+            cudaGraph_t graph = nullptr;
+            e = cudaStreamEndCapture(stream, &graph);
+            if (s != DELTA_OK) { if (graph) cudaGraphDestroy(graph); return s; }
+            if (e != cudaSuccess) return cuda_fail(h, e, "graph capture end");
+            h->graph_kernels = h->launches - before;
+            h->launches = before;
+            e = cudaGraphInstantiate(&h->gexec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                h->gexec = nullptr;
+                if (!h->pdl) return cuda_fail(h, e, "graph instantiate");
+                h->pdl = false;  // retry without programmatic edges
+            }
+        }
+        std::memcpy(h->gkey, key, sizeof key);
+        h->gbatch = batch;
+    }
+    cudaError_t e = cudaGraphLaunch(h->gexec, stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "graph launch");
+    h->launches += h->graph_kernels;
+    mark_step_done(h);
+    return DELTA_OK;
+}
+
+delta_status delta_decode_step_host(delta_t h, int32_t batch, const void* q_all_host, const void* k_all_host,
+                                    const void* v_all_host, float* out_all_host, cudaStream_t stream) {
+    if (!h) return fail(nullptr, DELTA_ERR_USAGE, "null handle");
+    if (batch < 1 || batch > h->cfg.max_batch) return fail(h, DELTA_ERR_USAGE, "batch out of range");
+    const delta_config& c = h->cfg;
+    const size_t e = elem_bytes(c);
+    const size_t qb = (size_t)c.num_layers * batch * c.num_q_heads * c.head_dim * e;
+    const size_t kb = (size_t)c.num_layers * batch * c.num_kv_heads * c.head_dim * e;
+    const size_t ob = (size_t)c.num_layers * batch * c.num_q_heads * c.head_dim * 4;
+    uint8_t* dq = h->at<uint8_t>(h->L.stage_q);
+    uint8_t* dk = h->at<uint8_t>(h->L.stage_k);
+    uint8_t* dv = h->at<uint8_t>(h->L.stage_v);
+    float* dout = h->at<float>(h->L.stage_out);
+    cudaError_t err = cudaMemcpyAsync(dq, q_all_host, qb, cudaMemcpyHostToDevice, stream);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(dk, k_all_host, kb, cudaMemcpyHostToDevice, stream);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(dv, v_all_host, kb, cudaMemcpyHostToDevice, stream);
+    if (err != cudaSuccess) return cuda_fail(h, err, "step_host H2D");
+    delta_status s = delta_decode_step(h, batch, dq, dk, dv, dout, nullptr, stream);
+    if (s != DELTA_OK) return s;
+    err = cudaMemcpyAsync(out_all_host, dout, ob, cudaMemcpyDeviceToHost, stream);
+    if (err != cudaSuccess) return cuda_fail(h, err, "step_host D2H");
+    return DELTA_OK;
+}
+
+delta_status delta_get_error(delta_t h, cudaStream_t stream, delta_status* sticky) {
+    if (!h || !sticky) return fail(h, DELTA_ERR_USAGE, "null argument");
+    cudaError_t e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "get_error sync");
+    int32_t v = 0;
+    int32_t* dev = h->at<int32_t>(h->L.err);
+    e = cudaMemcpy(&v, dev, sizeof v, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemset(dev, 0, sizeof v);
+    if (e != cudaSuccess) return cuda_fail(h, e, "get_error read");
+    *sticky = (delta_status)v;
+    return DELTA_OK;
+}
+
+delta_role delta_layer_role(delta_t h, int32_t layer) {
+    if (!h || layer < 0 || layer >= h->cfg.num_layers) return (delta_role)-1;
+    return (delta_role)h->role[layer];
+}
+
+int32_t delta_governing_layer(delta_t h, int32_t layer) {
+    if (!h || layer < 0 || layer >= h->cfg.num_layers) return -1;
+    return h->gov[layer];
+}
+
+int32_t delta_plan_capacity(delta_t h) { return h ? h->L.plan_cap : -1; }
+
+const char* delta_last_error_message(delta_t h) { return h ? h->msg.c_str() : g_msg.c_str(); }
+
+uint64_t delta_kernels_launched(delta_t h) { return h ? h->launches : 0; }
+
+}  // extern "C"

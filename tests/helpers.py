@@ -1,0 +1,218 @@
+"""Shared test harness: the same seeded synthetic inputs drive the CUDA path (through the
+C ABI) and the fp64 oracle.  Nothing here computes any of the method's arithmetic."""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+import oracle
+import synth
+
+# tolerance of the north star for bf16 KV with fp32 accumulation (R19)
+BF16_MAX_ABS, BF16_REL_L2 = 2e-3, 1e-2
+# fp32 KV (config C0): tighter (R19)
+FP32_MAX_ABS = 1e-5
+
+
+@dataclass
+class Shape:
+    L: int
+    m: int
+    g: int
+    d: int
+    F: int
+    delta: list
+    k: int
+    S: int
+    Lw: int
+    block: int
+    dtype: str  # "bf16" | "fp32"
+
+    def delta_config(self, max_batch, max_seq_len):
+        from paper_2510_09883_b200 import DELTA_BF16, DELTA_FP32, DeltaConfig
+        return DeltaConfig(num_layers=self.L, num_q_heads=self.m, num_kv_heads=self.g, head_dim=self.d,
+                           max_batch=max_batch, max_seq_len=max_seq_len, num_full_prefix=self.F,
+                           select_layers=list(self.delta), budget_k=self.k, n_sink=self.S, n_window=self.Lw,
+                           select_block=self.block, kv_dtype=DELTA_BF16 if self.dtype == "bf16" else DELTA_FP32)
+
+    def oracle_config(self):
+        return oracle.StackConfig(num_layers=self.L, m=self.m, g=self.g, d=self.d, page_size=16,
+                                  num_full_prefix=self.F, select_layers=list(self.delta), budget_k=self.k,
+                                  n_sink=self.S, n_window=self.Lw, select_block=self.block,
+                                  scale=float(np.float32(1.0 / np.sqrt(self.d))))
+
+
+C0 = Shape(L=4, m=8, g=2, d=64, F=1, delta=[1], k=128, S=4, Lw=32, block=1, dtype="fp32")
+C0_PAGE = Shape(L=4, m=8, g=2, d=64, F=1, delta=[1], k=128, S=4, Lw=32, block=16, dtype="fp32")
+C1 = Shape(L=32, m=32, g=8, d=128, F=2, delta=[2, 16, 25], k=2048, S=4, Lw=32, block=16, dtype="bf16")
+
+
+def planting_for(shape: Shape, s: int, kind: str = "planted"):
+    """Planted salient units inside the candidate region."""
+    blk = shape.block
+    lo = -(-shape.S // blk)
+    hi = (s - shape.Lw) // blk
+    if kind == "planted":
+        if blk == 1:
+            return synth.Planting(count=shape.k, block=1, B=3.0 if shape.d == 64 else 2.0, G=1.0, lo=lo, hi=hi)
+        return synth.Planting(count=shape.k // blk, block=blk, B=1.0, G=1.0, lo=lo, hi=hi)
+    if kind == "fewhot":  # 3 tokens whose logits are raised by ~+25 (attention-sink-like)
+        return synth.Planting(count=3, block=1, B=1.5, G=2.0 if shape.d == 64 else 1.5, lo=lo, hi=hi)
+    raise ValueError(kind)
+
+
+def oracle_layer(shape: Shape, seed: int, layer: int, seq: int, s: int, planting=None, want_alpha=False,
+                 tokens=None, nthreads=0):
+    """Oracle Eq.4 for one (layer, seq) on the generator's rows 0..s-1."""
+    K = synth.kv_rows(seed, layer, seq, 0, s, shape.g, shape.d, shape.dtype, "k", planting)
+    V = synth.kv_rows(seed, layer, seq, 0, s, shape.g, shape.d, shape.dtype, "v", planting)
+    kv = oracle.SeqKV.from_contiguous(K, V, 16)
+    q = synth.q_rows(seed, layer, seq, s, shape.m, shape.d, shape.dtype, planting)
+    scale = shape.oracle_config().scale
+    return oracle.decode_heads(q, kv, s if tokens is None else tokens, scale, want_alpha=want_alpha,
+                               nthreads=nthreads)
+
+
+def oracle_select(shape: Shape, alpha, s):
+    return oracle.select_from_alpha(shape.oracle_config(), alpha, s)
+
+
+def _candidates(s: int, shape: Shape) -> np.ndarray:
+    blk = shape.block
+    n_units = -(-s // blk)
+    forced = set()
+    if shape.S > 0:
+        forced |= set(range(0, (min(shape.S, s) - 1) // blk + 1))
+    if shape.Lw > 0:
+        forced |= set(range(max(0, s - shape.Lw) // blk, n_units))
+    return np.array(sorted(set(range(n_units)) - forced), dtype=np.int64)
+
+
+def boundary(keys: np.ndarray, s: int, shape: Shape):
+    """(k-th largest candidate key, relative gap to the (k+1)-th) from the ORACLE keys."""
+    cand = _candidates(s, shape)
+    k_units = shape.k // shape.block
+    if cand.size <= k_units or k_units == 0:
+        return None, float("inf")
+    srt = np.sort(keys[cand])[::-1]
+    return float(srt[k_units - 1]), float((srt[k_units - 1] - srt[k_units]) / max(srt[k_units - 1], 1e-300))
+
+
+def check_plan(gpu_units: np.ndarray, ora_units: np.ndarray, ora_keys: np.ndarray, s: int, shape: Shape,
+               exact: bool) -> bool:
+    """R20: exact equality when the oracle boundary gap exceeds 2e-5 (or `exact`, e.g. planted
+    inputs); otherwise differences only among units within 1e-5 (relative) of the boundary key.
+    Returns True if the two plans are identical."""
+    g, o = set(gpu_units.tolist()), set(ora_units.tolist())
+    bkey, gap = boundary(ora_keys, s, shape)
+    if exact or gap > 2e-5:
+        assert g == o, f"plan mismatch (gap {gap:.3g}): gpu-only {sorted(g - o)[:8]} oracle-only {sorted(o - g)[:8]}"
+        return True
+    for u in g ^ o:
+        assert abs(ora_keys[u] - bkey) <= 1e-5 * abs(bkey), f"unit {u} differs away from the boundary"
+    return g == o
+
+
+def assert_close_bf16(gpu: np.ndarray, ref: np.ndarray, what=""):
+    err = np.abs(gpu.astype(np.float64) - ref)
+    rel = np.linalg.norm(gpu.astype(np.float64) - ref) / max(np.linalg.norm(ref), 1e-30)
+    assert err.max() <= BF16_MAX_ABS, f"{what}: max abs {err.max():.3g} > {BF16_MAX_ABS}"
+    assert rel <= BF16_REL_L2, f"{what}: rel L2 {rel:.3g} > {BF16_REL_L2}"
+    return float(err.max()), float(rel)
+
+
+def assert_close_fp32(gpu: np.ndarray, ref: np.ndarray, what=""):
+    err = np.abs(gpu.astype(np.float64) - ref)
+    assert err.max() <= FP32_MAX_ABS, f"{what}: max abs {err.max():.3g} > {FP32_MAX_ABS}"
+    return float(err.max())
+
+
+class GpuCase:
+    """A DELTA stack on cuda:0 whose cache holds the generator's rows 0..s_pre-1 for every
+    (layer, sequence), laid out through a seeded scattered block table."""
+
+    def __init__(self, shape: Shape, seed: int, batch: int, s_pre: int, max_seq: int, planting=None):
+        import torch
+        from paper_2510_09883_b200 import DeltaStack
+        from synth import device as sd
+        self.shape, self.seed, self.batch, self.planting = shape, seed, batch, planting
+        self.cfg = shape.delta_config(batch, max_seq)
+        bt = torch.from_numpy(synth.block_table(seed, batch, self.cfg.max_pages))
+        self.stack = DeltaStack.allocate(self.cfg, bt)
+        sd.fill_pools(self.stack.k_pool, self.stack.v_pool, self.stack.block_table, seed, s_pre, batch,
+                      range(shape.L), planting)
+        self.stack.set_seq_lens([s_pre] * batch)
+        self.dt = torch.bfloat16 if shape.dtype == "bf16" else torch.float32
+
+    def inputs(self, s: int):
+        """Step inputs for the step whose cache holds s tokens after the append."""
+        import torch
+        from synth import device as sd
+        sh, B = self.shape, self.batch
+        q = torch.empty((sh.L, B, sh.m, sh.d), dtype=self.dt, device="cuda")
+        k = torch.empty((sh.L, B, sh.g, sh.d), dtype=self.dt, device="cuda")
+        v = torch.empty_like(k)
+        sd.fill_queries(q, self.seed, range(sh.L), [s] * B, self.planting)
+        sd.fill_new_kv(k, v, self.seed, range(sh.L), [s - 1] * B)
+        return q, k, v
+
+    def step_layers(self, s: int):
+        """One step through the per-layer ABI: fused append+decode, select after Delta layers."""
+        import torch
+        from paper_2510_09883_b200 import ROLE_SELECT
+        sh, B = self.shape, self.batch
+        q, k, v = self.inputs(s)
+        out = torch.empty((sh.L, B, sh.m, sh.d), dtype=torch.float32, device="cuda")
+        lse = torch.empty((sh.L, B, sh.m), dtype=torch.float32, device="cuda")
+        plans = {}
+        cap = self.stack.plan_capacity
+        for l in range(sh.L):
+            self.stack.append_decode_layer(l, k[l], v[l], q[l], out[l], lse[l])
+            if self.stack.role(l) == ROLE_SELECT:
+                idx = torch.empty((B, cap), dtype=torch.int32, device="cuda")
+                cnt = torch.empty((B,), dtype=torch.int32, device="cuda")
+                self.stack.select(l, B, idx_out=idx, count_out=cnt)
+                plans[l] = (idx, cnt)
+        torch.cuda.synchronize()
+        host_plans = {l: [idx[b, : int(cnt[b])].cpu().numpy() for b in range(B)] for l, (idx, cnt) in plans.items()}
+        return out.cpu().numpy(), lse.cpu().numpy(), host_plans
+
+    def step_graph(self, s: int, stream=None):
+        import torch
+        sh, B = self.shape, self.batch
+        q, k, v = self.inputs(s)
+        out = torch.empty((sh.L, B, sh.m, sh.d), dtype=torch.float32, device="cuda")
+        lse = torch.empty((sh.L, B, sh.m), dtype=torch.float32, device="cuda")
+        st = stream or torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            self.stack.decode_step(q, k, v, out, lse, stream=st)
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        return out.cpu().numpy(), lse.cpu().numpy()
+
+
+def oracle_step(shape: Shape, seed: int, seq: int, s: int, layers=None, planting=None):
+    """Oracle results for the given layers of one sequence (all layers by default); Delta
+    layers needed by requested sparse layers are evaluated too.  Returns
+    {layer: (out, lse, units|None, keys|None, tokens|None)}."""
+    roles, gov = oracle.validate_tiers(shape.L, shape.F, shape.delta)
+    want = set(range(shape.L)) if layers is None else set(layers)
+    need = set(want) | {int(gov[l]) for l in want if roles[l] == oracle.ROLE_SPARSE}
+    res, plans = {}, {}
+    for l in sorted(need):
+        if roles[l] == oracle.ROLE_FULL:
+            out, lse, _ = oracle_layer(shape, seed, l, seq, s, planting)
+            res[l] = (out, lse, None, None, None)
+        elif roles[l] == oracle.ROLE_SELECT:
+            out, lse, alpha = oracle_layer(shape, seed, l, seq, s, planting, want_alpha=True)
+            keys, units = oracle_select(shape, alpha, s)
+            plans[l] = units
+            res[l] = (out, lse, units, keys, None)
+    for l in sorted(need):
+        if roles[l] == oracle.ROLE_SPARSE:
+            toks = oracle.units_to_tokens(plans[int(gov[l])], shape.block, s)
+            out, lse, _ = oracle_layer(shape, seed, l, seq, s, planting, tokens=toks)
+            res[l] = (out, lse, None, None, toks)
+    return res

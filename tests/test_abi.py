@@ -1,0 +1,83 @@
+"""The C-ABI boundary, on CPU: the library loads without a GPU, exports every function
+include/delta.h declares, and its host-side validation (schedule, shapes, budget) follows
+the paper's problem statement."""
+import ctypes
+import json
+import os
+
+import pytest
+
+import paper_2510_09883_b200 as d200
+from paper_2510_09883_b200 import DeltaConfig, DeltaError
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    lib = d200.load_library()
+    names = d200.declared_functions()
+    assert {"delta_create", "delta_append_kv", "delta_decode_layer", "delta_select", "delta_destroy"} <= set(names)
+    for n in names:
+        assert hasattr(lib, n), f"{n} declared in include/delta.h but not exported"
+    assert lib.delta_version().decode().startswith("delta-b200")
+
+
+def test_no_product_dependency_on_oracle():
+    """The product path never imports or links the oracle (they share no code)."""
+    pkg = os.path.dirname(d200.__file__)
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(root, f)).read()
+                for bad in ("import oracle", "from oracle", "delta_oracle", "oracle_"):
+                    assert bad not in src, (f, bad)
+    syms = os.popen(f"nm -D {d200.binding.LIB_PATH}").read()
+    assert "oracle_" not in syms and "delta_create" in syms
+
+
+def _c1(**kw):
+    base = dict(num_layers=32, num_q_heads=32, num_kv_heads=8, head_dim=128, max_batch=1, max_seq_len=32768 + 64,
+                num_full_prefix=2, select_layers=[2, 16, 25], budget_k=2048, n_sink=4, n_window=32, select_block=16)
+    base.update(kw)
+    return DeltaConfig(**base)
+
+
+def test_query_sizes_c1():
+    pool, ws = d200.query_sizes(_c1())
+    # one pool = L x pages x g x P x d x 2 bytes
+    assert pool == 32 * 2052 * 8 * 16 * 128 * 2
+    assert ws > 0 and ws % 256 == 0
+
+
+@pytest.mark.parametrize("ex", GOLD["tiers"], ids=lambda e: e["cite"][:14])
+def test_tier_validation_matches_paper(ex):
+    cfg = _c1(num_layers=ex["num_layers"], num_full_prefix=ex["F"], select_layers=ex["delta"])
+    if ex["ok"]:
+        d200.query_sizes(cfg)
+    else:
+        with pytest.raises(DeltaError, match="CONFIG"):
+            d200.query_sizes(cfg)
+
+
+@pytest.mark.parametrize("bad", [
+    dict(num_kv_heads=7),                       # g must divide m
+    dict(head_dim=96),                          # d in {64, 128}
+    dict(page_size=8),                          # P = 16
+    dict(budget_k=2040),                        # page mode needs P | k (R6)
+    dict(select_block=4),                       # token (1) or page (P) granularity
+    dict(num_q_heads=64, num_kv_heads=2),       # gs <= 16
+    dict(select_layers=[16, 2, 25]),            # ascending
+    dict(num_full_prefix=3),                    # Delta layer 2 inside the full prefix
+    dict(shard_world=2),                        # not built
+])
+def test_config_errors(bad):
+    with pytest.raises(DeltaError, match="CONFIG"):
+        d200.query_sizes(_c1(**bad))
+
+
+def test_null_handle_calls_are_usage_errors():
+    lib = d200.load_library()
+    assert lib.delta_decode_layer(None, 0, 1, None, None, None, None) == 2
+    assert lib.delta_select(None, 0, 1, None, None, None, None) == 2
+    assert lib.delta_layer_role(None, 0) == -1
+    assert lib.delta_destroy(None) == 2
