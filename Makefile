@@ -29,3 +29,20 @@ clean:
 	rm -rf $(BUILD) $(PKG)/libdelta.so synth/libsynth.so oracle/liboracle.so
 
 .PHONY: all clean
+
+# Latency-trace variant (globaltimer phase stamps per CTA) for tools/trace_probe.py; not the product.
+TRACE_OBJS := $(patsubst $(BUILD)/%.o,build_trace/%.o,$(OBJS))
+build_trace:
+	mkdir -p build_trace
+build_trace/%.o: $(CSRC)/%.cu $(HDRS) | build_trace
+	$(NVCC) $(NVFLAGS) -DDELTA_TRACE -c $< -o $@ 2> /dev/null
+build_trace/libdelta.so: $(TRACE_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(TRACE_OBJS)
+trace: build_trace/libdelta.so
+.PHONY: trace
+
+# Experiment variants of the trace build (kernel-cost breakdown); not the product.
+build_exp_%/libdelta.so: $(CSRC)/*.cu $(HDRS)
+	mkdir -p build_exp_$*
+	for f in attn_tc attn_simt select append delta_api; do $(NVCC) $(NVFLAGS) -DDELTA_TRACE -DEXP_$* -c $(CSRC)/$$f.cu -o build_exp_$*/$$f.o 2>/dev/null || exit 1; done
+	$(NVCC) $(ARCH) -shared -o $@ build_exp_$*/*.o

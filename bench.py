@@ -26,7 +26,6 @@ import json
 import math
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -56,54 +55,47 @@ def log(*a):
 
 # ------------------------------------------------------------------ clocks sampling
 class ClockSampler:
+    """Samples SM clock and clock-event (throttle) reasons through NVML every ~2 ms while the
+    timed region runs (nvidia-smi's 100 ms floor is longer than a short timed region)."""
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
+        self.sm, self.bits = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.t = None
+        self.err = None
+
+    def _run(self):
+        import pynvml
+        try:
+            pynvml.nvmlInit()
+            hd = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(hd, pynvml.NVML_CLOCK_SM))
+            while True:
+                self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(hd, pynvml.NVML_CLOCK_SM)))
+                self.bits |= int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(hd))
+                if self._stop.wait(0.002):
+                    break
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
-                text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm, mx, reasons = [], None, set()
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 3:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-                bits = int(parts[2], 16) if parts[2].startswith("0x") else int(parts[2])
-            except ValueError:
-                continue
-            for bit, name in self.REASONS.items():
-                if bits & bit and name != "gpu_idle":
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        self._stop.set()
+        if self.t is not None:
+            self.t.join(timeout=5)
+        if self.err and not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"nvml unavailable: {self.err}"], "samples": 0}
+        reasons = sorted(n for bit, n in self.REASONS.items() if self.bits & bit and n != "gpu_idle")
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.sm), "source": "NVML, 2 ms period, during the timed region"}
 
 
 def measured_peaks():
@@ -263,12 +255,12 @@ def run_ours(args, c):
     # the Full stack shares the pools and block table (same library, every layer FULL)
     fcfg = make_cfg(True)
     _, fws = d200.query_sizes(fcfg)
-    full = d200.DeltaStack(fcfg, delta.k_pool, delta.v_pool, delta.block_table,
+    full = d200.DeltaStack(fcfg, delta.kv_pool, delta.block_table,
                            torch.zeros(fws, dtype=torch.uint8, device=dev))
     t0 = time.time()
-    sd.fill_pools(delta.k_pool, delta.v_pool, delta.block_table, seed, s_pre, batch, range(c["L"]))
+    sd.fill_pools(delta.kv_pool, delta.block_table, seed, s_pre, batch, range(c["L"]))
     torch.cuda.synchronize()
-    log(f"[rank {rank}] filled {2 * delta.k_pool.numel() * 2 / 2**30:.1f} GiB KV in {time.time() - t0:.1f}s "
+    log(f"[rank {rank}] filled {delta.kv_pool.numel() * 2 / 2**30:.1f} GiB KV in {time.time() - t0:.1f}s "
         f"(batch {batch}, s_pre {s_pre})")
 
     L_, m, g, d = c["L"], c["m"], c["g"], c["d"]
@@ -363,21 +355,38 @@ def run_ours(args, c):
     h2d = (qh[0].numel() + kh[0].numel() + vh[0].numel()) * 2
     d2h = oh.numel() * 4
 
-    # ---- roofline: dominant kernel = full-cache decode of one layer (timed alone, eager)
-    reps = 20
-    delta.set_seq_lens([s_first] * batch)
-    lay = 0  # a FULL layer
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    with torch.cuda.stream(stream):
-        for _ in range(3):
-            delta.decode_layer(lay, q_all[W, lay], out[lay], stream=stream)
-        ev[0].record(stream)
-        for _ in range(reps):
-            delta.decode_layer(lay, q_all[W, lay], out[lay], stream=stream)
-        ev[1].record(stream)
-    stream.synchronize()
-    us_kernel = ev[0].elapsed_time(ev[1]) * 1e3 / reps
-    kbytes = batch * s_first * g * d * 2 * 2
+    # ---- per-kernel timings, eager launches on `stream` (CUDA events on that stream).  The
+    # state after the last e2e step is a consistent decode step at s_last, so every role may
+    # be re-run without an append: FULL (layer 0), SELECT decode + delta_select (first Delta
+    # layer), SPARSE (the layer after it, reusing that Delta layer's plan).
+    s_last = s_first + K - 1
+    reps = 50
+
+    def time_calls(fn):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with torch.cuda.stream(stream):
+            for _ in range(5):
+                fn()
+            ev[0].record(stream)
+            for _ in range(reps):
+                fn()
+            ev[1].record(stream)
+        stream.synchronize()
+        return ev[0].elapsed_time(ev[1]) * 1e3 / reps
+
+    dl = c["delta"][0]
+    sp = dl + 1
+    qW = q_all[W + K - 1]
+    us_full = time_calls(lambda: delta.decode_layer(0, qW[0], out[0], stream=stream))
+    us_sel_dec = time_calls(lambda: delta.decode_layer(dl, qW[dl], out[dl], stream=stream))
+    us_select = time_calls(lambda: delta.select(dl, batch, stream=stream))
+    us_sparse = time_calls(lambda: delta.decode_layer(sp, qW[sp], out[sp], stream=stream))
+    err = delta.get_error()
+    assert err == 0, f"device error flag {err} after per-kernel timing"
+    kbytes = batch * s_last * g * d * 2 * 2
+    n_sp_tok = sparse_token_count(s_last, c["k"])
+    sp_bytes = batch * (n_sp_tok * g * d * 2 * 2 + (n_sp_tok // PAGE) * 4)
+    us_kernel = us_full
     peak, peak_src = measured_peaks()
     achieved = kbytes / (us_kernel * 1e-6) / 1e9
     traffic = None
@@ -387,11 +396,15 @@ def run_ours(args, c):
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-
-    # sparse-layer kernel (secondary): plan from the last step, timed alone
+    kernels = {
+        "full_layer_us": round(us_full, 3), "full_layer_gbs": round(kbytes / (us_full * 1e-6) / 1e9, 1),
+        "select_layer_decode_us": round(us_sel_dec, 3), "select_topk_us": round(us_select, 3),
+        "sparse_layer_us": round(us_sparse, 3), "sparse_layer_gbs": round(sp_bytes / (us_sparse * 1e-6) / 1e9, 1),
+        "sparse_layer_bytes": sp_bytes, "note": "eager launches back to back (PDL), %d reps, s=%d" % (reps, s_last),
+    }
     if rank == 0:
         log(f"DELTA {1e3 * ms_delta / K:.1f} us/step, Full {1e3 * ms_full / K:.1f} us/step, "
-            f"speedup {ms_full / ms_delta:.3f}x; full-layer kernel {us_kernel:.2f} us = {achieved:.0f} GB/s")
+            f"speedup {ms_full / ms_delta:.3f}x; kernels {kernels}")
 
     if rank != 0:
         if world > 1:
@@ -424,9 +437,10 @@ def run_ours(args, c):
         "full_stack_gbs": round(byts_full * world / (ms_full * 1e-3) / 1e9, 2),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "attn_tc_kernel<128,false> FULL, one layer, s=%d" % s_first,
+                     "kernel": "attn_tc_kernel<128,false> FULL, one layer, s=%d" % s_last,
                      "algorithmic_bytes_per_launch": kbytes, "avg_launch_us": round(us_kernel, 3),
                      "peak_source": peak_src},
+        "kernels": kernels,
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": round(ms_e2e / K, 5)},
         "gpu_launches": int(launches),
@@ -442,7 +456,7 @@ def run_ours(args, c):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))

@@ -80,9 +80,10 @@ typedef struct {
 
 /* Caller-owned device buffers.  Sizes from delta_query_sizes. */
 typedef struct {
-    void* k_pool;              /* [L][num_phys_pages][g][P][d] kv_dtype: one "head-page" of P*d
-                                  contiguous elements per (layer, page, kv head) */
-    void* v_pool;              /* same layout */
+    void* kv_pool;             /* [L][num_phys_pages][g][2][P][d] kv_dtype, 1024-byte aligned:
+                                  for every (layer, page, kv head) the P key rows then the P
+                                  value rows, 2*P*d contiguous elements, so one request moves
+                                  a head's K and V of a page (PAPER.md:180-181 paging, P = 16) */
     const int32_t* block_table;/* [max_batch][ceil(max_seq_len/P)] int32 physical page ids,
                                   shared by all layers: token t of sequence b lives in page
                                   block_table[b][t/P], slot t%P (PAPER.md:181 p(t)) */
@@ -91,9 +92,9 @@ typedef struct {
     size_t workspace_bytes;
 } delta_buffers;
 
-/* Byte sizes of one pool (K or V) and of the workspace for this config on the CURRENT
- * device.  CONFIG error if the config is invalid. */
-delta_status delta_query_sizes(const delta_config* cfg, size_t* pool_bytes_each,
+/* Byte sizes of kv_pool and of the workspace for this config on the CURRENT device.
+ * CONFIG error if the config is invalid. */
+delta_status delta_query_sizes(const delta_config* cfg, size_t* kv_pool_bytes,
                                size_t* workspace_bytes);
 
 /* Validate the config (shapes, schedule as in SPEC.md:378-386, budget), compute each

@@ -12,7 +12,9 @@ import re
 from dataclasses import dataclass, field
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdelta.so")
+# DELTA_LIB_PATH selects an instrumented build of the SAME sources (make trace) for latency
+# analysis; the product library is the in-tree libdelta.so.
+LIB_PATH = os.environ.get("DELTA_LIB_PATH") or os.path.join(_HERE, "libdelta.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "delta.h")
 
 DELTA_BF16, DELTA_FP32 = 0, 1
@@ -39,7 +41,7 @@ class _Config(ctypes.Structure):
 
 
 class _Buffers(ctypes.Structure):
-    _fields_ = [("k_pool", ctypes.c_void_p), ("v_pool", ctypes.c_void_p), ("block_table", ctypes.c_void_p),
+    _fields_ = [("kv_pool", ctypes.c_void_p), ("block_table", ctypes.c_void_p),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
 
 
@@ -168,30 +170,40 @@ def _stream(stream) -> int:
 class DeltaStack:
     """One handle of the DELTA decode-attention stack over caller-owned torch buffers."""
 
-    def __init__(self, cfg: DeltaConfig, k_pool, v_pool, block_table, workspace):
+    def __init__(self, cfg: DeltaConfig, kv_pool, block_table, workspace):
+        """kv_pool: [L][phys_pages][g][2][P][d] (K rows then V rows per (page, head))."""
         self.cfg = cfg
         self.lib = load_library()
-        self.k_pool, self.v_pool, self.block_table, self.workspace = k_pool, v_pool, block_table, workspace
+        self.kv_pool, self.block_table, self.workspace = kv_pool, block_table, workspace
         c, self._keep = cfg.to_c()
-        b = _Buffers(k_pool.data_ptr(), v_pool.data_ptr(), block_table.data_ptr(), workspace.data_ptr(),
+        b = _Buffers(kv_pool.data_ptr(), block_table.data_ptr(), workspace.data_ptr(),
                      workspace.numel() * workspace.element_size())
         h = ctypes.c_void_p()
         _check(self.lib.delta_create(ctypes.byref(c), ctypes.byref(b), ctypes.byref(h)))
         self.h = h
 
+    @property
+    def k_pool(self):
+        """View [L][phys_pages][g][P][d] of the key rows of kv_pool."""
+        return self.kv_pool[:, :, :, 0]
+
+    @property
+    def v_pool(self):
+        """View [L][phys_pages][g][P][d] of the value rows of kv_pool."""
+        return self.kv_pool[:, :, :, 1]
+
     @classmethod
     def allocate(cls, cfg: DeltaConfig, block_table, device="cuda"):
-        """Allocate pools + workspace with torch (1024-byte aligned) and create the handle."""
+        """Allocate kv_pool + workspace with torch (1024-byte aligned) and create the handle."""
         import torch
         pool_bytes, ws_bytes = query_sizes(cfg)
         dt = torch.bfloat16 if cfg.kv_dtype == DELTA_BF16 else torch.float32
-        shape = (cfg.num_layers, cfg.phys_pages, cfg.num_kv_heads, cfg.page_size, cfg.head_dim)
-        k_pool = torch.zeros(shape, dtype=dt, device=device)
-        v_pool = torch.zeros(shape, dtype=dt, device=device)
-        assert k_pool.numel() * k_pool.element_size() == pool_bytes
+        shape = (cfg.num_layers, cfg.phys_pages, cfg.num_kv_heads, 2, cfg.page_size, cfg.head_dim)
+        kv_pool = torch.zeros(shape, dtype=dt, device=device)
+        assert kv_pool.numel() * kv_pool.element_size() == pool_bytes
         ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=device)
         bt = block_table.to(device=device, dtype=torch.int32).contiguous()
-        return cls(cfg, k_pool, v_pool, bt, ws)
+        return cls(cfg, kv_pool, bt, ws)
 
     # ------------------------------------------------------------------ calls
     def set_seq_lens(self, lens, layer: int = -1, stream=None):

@@ -10,7 +10,7 @@ namespace {
 __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
     const int b = blockIdx.x;
     pdl_wait();
-    const int n = p.seq_len[p.layer * p.max_batch + b];
+    const int n = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
     if (n + p.ntok > p.max_seq) {
         if (threadIdx.x == 0) set_err(p.err, kDevCapacity);
         return;
@@ -26,17 +26,17 @@ __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
         const int hh = (i / chunks) % p.g;
         const int tok = i / (chunks * p.g);
         const int t = n + tok;
-        const size_t row = (((size_t)p.layer * p.num_phys + bt[t / kPage]) * p.g + hh) * kPage + (t % kPage);
+        const size_t row = kv_row((size_t)p.layer * p.num_phys + bt[t / kPage], p.g, hh, t % kPage);
         const size_t src_off = ((size_t)tok * p.g + hh) * row_bytes + (size_t)c * 16;
         const size_t dst_off = row * row_bytes + (size_t)c * 16;
-        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.k_pool) + dst_off) =
-            *reinterpret_cast<const uint4*>(ks + src_off);
-        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.v_pool) + dst_off) =
+        uint8_t* pool = reinterpret_cast<uint8_t*>(p.kv_pool);
+        *reinterpret_cast<uint4*>(pool + dst_off) = *reinterpret_cast<const uint4*>(ks + src_off);
+        *reinterpret_cast<uint4*>(pool + dst_off + (size_t)kPage * row_bytes) =
             *reinterpret_cast<const uint4*>(vs + src_off);
     }
     __syncthreads();
     pdl_launch_dependents();
-    if (threadIdx.x == 0) p.seq_len[p.layer * p.max_batch + b] = n + p.ntok;
+    if (threadIdx.x == 0) p.seq_len[p.layer * p.max_batch + b] = (n + p.ntok) * p.g;
 }
 
 }  // namespace

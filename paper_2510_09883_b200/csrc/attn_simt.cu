@@ -26,15 +26,15 @@ template <typename T, int D>
 __global__ void __launch_bounds__(NW * 32) attn_simt_kernel(const AttnParams p) {
     constexpr int VPL = D / 32;
     __shared__ float ms[NW * 16], ls[NW * 16];
-    __shared__ float os[NW * 16 * D];
-    __shared__ int sflag;
+    __shared__ __align__(16) float os[NW * 16 * os_stride<D>()];
+    __shared__ __align__(16) float cstage[ClusterStage<D>::kFloats];  // peers push partials here
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int gs = p.gs;
     pdl_wait();
 
-    const int n_old = p.seq_len[p.layer * p.max_batch + b];
+    const int n_old = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
     const int s = p.fuse_append ? n_old + 1 : n_old;
     const bool cap_err = s > p.max_seq;
     const bool token_plan = (p.role == kRoleSparse) && p.sel_block == 1;
@@ -56,16 +56,15 @@ __global__ void __launch_bounds__(NW * 32) attn_simt_kernel(const AttnParams p) 
     const int32_t* bt = p.block_table + (size_t)b * p.bt_stride;
     const int32_t* plan = p.plan_idx + (size_t)b * p.plan_cap;
     const size_t layer_ph = (size_t)p.layer * p.num_phys;
-    const T* kpool = reinterpret_cast<const T*>(p.k_pool);
-    const T* vpool = reinterpret_cast<const T*>(p.v_pool);
+    const T* pool = reinterpret_cast<const T*>(p.kv_pool);
     const T* k_new = reinterpret_cast<const T*>(p.k_new) + ((size_t)b * p.g + h) * D;
     const T* v_new = reinterpret_cast<const T*>(p.v_new) + ((size_t)b * p.g + h) * D;
 
     if (p.fuse_append && !cap_err && split == 0 && warp == 0) {  // Eq.7 append of head h
         const int t = s - 1;
-        const size_t row = ((layer_ph + bt[t / kPage]) * p.g + h) * kPage + (t % kPage);
-        T* kd = reinterpret_cast<T*>(p.k_pool) + row * D;
-        T* vd = reinterpret_cast<T*>(p.v_pool) + row * D;
+        const size_t row = kv_row(layer_ph + bt[t / kPage], p.g, h, t % kPage);
+        T* kd = reinterpret_cast<T*>(p.kv_pool) + row * D;
+        T* vd = kd + kPage * D;
         for (int e = lane; e < D; e += 32) { kd[e] = k_new[e]; vd[e] = v_new[e]; }
     }
 
@@ -101,8 +100,8 @@ __global__ void __launch_bounds__(NW * 32) attn_simt_kernel(const AttnParams p) 
             if (p.fuse_append && t == s - 1) {
                 kr = k_new; vr = v_new;
             } else {
-                const size_t row = ((layer_ph + bt[t / kPage]) * p.g + h) * kPage + (t % kPage);
-                kr = kpool + row * D; vr = vpool + row * D;
+                const size_t row = kv_row(layer_ph + bt[t / kPage], p.g, h, t % kPage);
+                kr = pool + row * D; vr = kr + kPage * D;
             }
             float kv[VPL], vv[VPL];
 #pragma unroll
@@ -135,27 +134,39 @@ __global__ void __launch_bounds__(NW * 32) attn_simt_kernel(const AttnParams p) 
         if (j >= gs) break;
         if (lane == 0) { ms[warp * 16 + j] = mj[j]; ls[warp * 16 + j] = lj[j]; }
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) os[(warp * 16 + j) * D + lane * VPL + v] = o[j][v];
+        for (int v = 0; v < VPL; ++v) os[(warp * 16 + j) * os_stride<D>() + lane * VPL + v] = o[j][v];
     }
     __syncthreads();
     pdl_launch_dependents();
-    cta_merge<D>(p, ms, ls, os, NW, b, h, split, tid, NW * 32);
-    grid_combine<D>(p, b, h, s, stale, cap_err, tid, NW * 32, &sflag);
+    cluster_epilogue<D, NW>(p, ms, ls, os, cstage, b, h, stale, cap_err, s);
 }
 
 template <typename T, int D>
-cudaError_t launch_impl(const AttnParams& p, cudaStream_t st, bool pdl) {
+cudaError_t launch_impl(const AttnParams& p0, cudaStream_t st, bool pdl) {
+    auto kern = attn_simt_kernel<T, D>;
+    static int max_cluster = 0;
+    if (max_cluster == 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        max_cluster = cluster_limit((const void*)kern, NW * 32, 0);
+    }
+    AttnParams p = p0;
+    p.nsplit = p.nsplit < max_cluster ? p.nsplit : max_cluster;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.nsplit, p.g, p.batch);
     cfg.blockDim = dim3(NW * 32);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.nsplit;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, attn_simt_kernel<T, D>, p);
+    cfg.numAttrs = pdl ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 }  // namespace

@@ -21,40 +21,64 @@
 //  * fused append (Eq.7): split 0 writes the new K/V row to the pool;
 //    the warp whose tile holds token s-1 patches it into shared memory from the input.
 //  * end: warps merge (cta_merge), last CTA per (b, h) merges splits (grid_combine).
+#include <algorithm>
+
 #include "combine.cuh"
+
+#ifdef DELTA_TRACE
+extern "C" int delta_trace_read(void* host, size_t bytes) {  // copies then clears the stamps
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess)
+        e = cudaMemcpyFromSymbol(host, g_delta_trace, bytes < sizeof(g_delta_trace) ? bytes : sizeof(g_delta_trace));
+    void* dev = nullptr;
+    if (e == cudaSuccess) e = cudaGetSymbolAddress(&dev, g_delta_trace);
+    if (e == cudaSuccess) e = cudaMemset(dev, 0, sizeof(g_delta_trace));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    return (int)e;
+}
+#endif
 
 namespace delta {
 namespace {
 
 constexpr int NCW = 4;      // consumer warps
-constexpr int NSTAGE = 3;   // pipeline depth (stages of NCW head-pages)
 constexpr int kThreads = (NCW + 1) * 32;
+// pipeline depth (stages of NCW head-pages): kDeep when one CTA per SM (few CTAs, e.g. batch
+// 1), kShallow when two CTAs share an SM.
+constexpr int kDeep = 6, kShallow = 3;
 
-template <int D>
+template <int D, int NSTAGE>
 struct TcCfg {
-    static constexpr int kTile = kPage * D * 2;        // bytes of one head-page
-    static constexpr int kStageBytes = NCW * kTile;    // per tensor per stage
-    static constexpr int kRing = NSTAGE * kStageBytes; // per tensor
-    static constexpr int kSmem = 1024 + 2 * kRing + 2 * NSTAGE * 8 + 16;
+    static constexpr int kHalf = kPage * D * 2;        // bytes of one head-page of K (or of V)
+    static constexpr int kTile = 2 * kHalf;            // K then V of one (page, head): one TMA request
+    static constexpr int kRing = NSTAGE * NCW * kTile;
+    static constexpr int kRowTok = NSTAGE * NCW * kPage;  // token id of every ring row (-1 = none)
+    static constexpr int kSmem = 1024 + kRing + ClusterStage<D>::kBytes + 2 * NSTAGE * 8 + kRowTok * 4 + 16;
 };
 
-// byte offset of 16-byte chunk c (0..D/8-1) of row r inside a 128B-swizzled head-page
+// Byte offset of 16-byte chunk c (0..D/8-1) of row r inside a 128B-swizzled head-page as
+// one TMA box writes it.  D = 64: 16 rows of 128 B.  D = 128: the box is 3-D {64, 2, 16}
+// (one 4 KiB request per head-page), so row r's two 128-byte halves are consecutive
+// 128-byte lines 2r and 2r+1; the 128B swizzle XORs the chunk with the line index mod 8.
+template <int D>
 __device__ __forceinline__ uint32_t swz(int r, int c) {
-    return (uint32_t)((c >> 3) * (kPage * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+    if (D == 64) return (uint32_t)(r * 128 + (((c & 7) ^ (r & 7)) << 4));
+    const int line = 2 * r + (c >> 3);
+    return (uint32_t)(line * 128 + (((c & 7) ^ (line & 7)) << 4));
 }
 
-template <int D, bool TOKEN_PLAN>
-__global__ void __launch_bounds__(kThreads, 2)
-attn_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-               const AttnParams p) {
-    using C = TcCfg<D>;
+template <int D, bool TOKEN_PLAN, int NSTAGE, int NH>
+__global__ void __launch_bounds__(kThreads, 1)
+attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
+    using C = TcCfg<D, NSTAGE>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* kbuf = base;
-    uint8_t* vbuf = base + C::kRing;
-    uint64_t* full = reinterpret_cast<uint64_t*>(vbuf + C::kRing);
+    uint8_t* ring = base;  // [NSTAGE][NCW] tiles of kTile bytes: K rows then V rows
+    float* cstage = reinterpret_cast<float*>(ring + C::kRing);  // peers push partials here
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + C::kRing + ClusterStage<D>::kBytes);
     uint64_t* empty = full + NSTAGE;
-    int* sflag = reinterpret_cast<int*>(empty + NSTAGE);
+    int* rowtok = reinterpret_cast<int*>(empty + NSTAGE);  // [NSTAGE][NCW][P], written by the producer
+    int* sflag = rowtok + C::kRowTok;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -67,14 +91,21 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__
         fence_mbar_init();
     }
     if (!TOKEN_PLAN && warp == NCW && lane == 0) {
-        tma_prefetch_desc(&tm_k);
-        tma_prefetch_desc(&tm_v);
+        tma_prefetch_desc(&tm_kv);
     }
     __syncthreads();
-    pdl_wait();  // everything below reads state written by earlier launches
+    if (tid == 0) DTRACE(0);
+    // Programmatic dependent launch: without `prewait` everything waits for the previous
+    // kernel here.  With `prewait` (the host knows the previous kernel of this handle wrote
+    // neither this layer's length counter nor the plan read here) the geometry and the KV
+    // stream start before the wait — the cache rows < s-1, the block table and the plan are
+    // then at least two kernels old, hence complete — and only the consumers (q, k_new, v_new,
+    // outputs) wait, so the first stages land while the previous layer finishes.
+    if (!p.prewait) pdl_wait();
+    if (tid == 0) DTRACE(1);
 
     // ---------------------------------------------------------------- geometry
-    const int n_old = p.seq_len[p.layer * p.max_batch + b];
+    const int n_old = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
     const int s = p.fuse_append ? n_old + 1 : n_old;
     const bool cap_err = s > p.max_seq;
     bool stale = false;
@@ -94,74 +125,114 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__
     }
     const int32_t* bt = p.block_table + (size_t)b * p.bt_stride;
     const int32_t* plan = p.plan_idx + (size_t)b * p.plan_cap;
+    const int32_t* plan_phys = p.plan_phys + (size_t)b * p.plan_cap;
     const size_t layer_ph = (size_t)p.layer * p.num_phys;
+    if (p.prewait && warp != NCW) pdl_wait();
     const __nv_bfloat16* k_new = reinterpret_cast<const __nv_bfloat16*>(p.k_new) + ((size_t)b * p.g + h) * D;
     const __nv_bfloat16* v_new = reinterpret_cast<const __nv_bfloat16*>(p.v_new) + ((size_t)b * p.g + h) * D;
 
-    // fused append: split 0 writes the new row of head h to the pools (Eq.7)
+    // fused append: split 0 writes the new row of head h to the pool (Eq.7)
     if (p.fuse_append && !cap_err && split == 0 && warp == 0) {
         constexpr int kChunks = D / 8;
         const int t = s - 1;
-        const size_t row = ((layer_ph + bt[t / kPage]) * p.g + h) * kPage + (t % kPage);
+        const size_t krow = kv_row(layer_ph + bt[t / kPage], p.g, h, t % kPage);
+        __nv_bfloat16* pool = reinterpret_cast<__nv_bfloat16*>(p.kv_pool);
         if (lane < kChunks) {
-            reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.k_pool) + row * D)[lane] =
-                reinterpret_cast<const uint4*>(k_new)[lane];
+            reinterpret_cast<uint4*>(pool + krow * D)[lane] = reinterpret_cast<const uint4*>(k_new)[lane];
         } else if (lane < 2 * kChunks) {
-            reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.v_pool) + row * D)[lane - kChunks] =
+            reinterpret_cast<uint4*>(pool + (krow + kPage) * D)[lane - kChunks] =
                 reinterpret_cast<const uint4*>(v_new)[lane - kChunks];
         }
     }
 
+    // warp states for the epilogue live in the ring once every consumer is done with it
+    float* ms = reinterpret_cast<float*>(ring);
+    float* ls = ms + NCW * 16;
+    float* os = ls + NCW * 16;
+    static_assert((2 * NCW * 16 + NCW * 16 * os_stride<D>()) * 4 <= TcCfg<D, NSTAGE>::kRing,
+                  "epilogue state must fit in the K ring");
+
     if (warp == NCW) {
         // ============================================================ producer
+        // The whole warp resolves up to 32 tiles' page ids (or 64 rows' token ids) with
+        // independent loads, so the dependent plan -> block-table -> copy chain costs two
+        // L2 round trips per batch rather than per tile.  The token id of every ring row is
+        // handed to the consumers through shared memory (published by the stage barrier).
         if (!TOKEN_PLAN) {
-            if (lane == 0) {
-                for (int it = 0, iter = 0; it < n_items; it += NCW, ++iter) {
+            for (int base = 0; base < n_items; base += 32) {
+                int my_lp = -1, my_phys = 0;
+                if (base + lane < n_items) {
+                    if (p.role == kRoleSparse) {  // logical and physical page: independent loads
+                        my_lp = plan[unit0 + base + lane];
+                        my_phys = plan_phys[unit0 + base + lane];
+                    } else {
+                        my_lp = unit0 + base + lane;
+                        my_phys = bt[my_lp];
+                    }
+                }
+                const int nb = min(32, n_items - base);
+                for (int j = 0; j < nb; j += NCW) {
+                    const int iter = (base + j) / NCW;
                     const int stg = iter % NSTAGE, round = iter / NSTAGE;
                     if (round > 0) mbar_wait(&empty[stg], (round - 1) & 1);
-                    const int valid = min(NCW, n_items - it);
-                    mbar_arrive_expect_tx(&full[stg], valid * 2 * C::kTile);
-                    for (int w = 0; w < valid; ++w) {
-                        const int item = it + w;
-                        const int lp = (p.role == kRoleSparse) ? plan[unit0 + item] : unit0 + item;
-                        const int row0 = (int)(((layer_ph + bt[lp]) * p.g + h) * kPage);
-                        uint8_t* kd = kbuf + (stg * NCW + w) * C::kTile;
-                        uint8_t* vd = vbuf + (stg * NCW + w) * C::kTile;
+                    const int valid = min(NCW, nb - j);
 #pragma unroll
-                        for (int half = 0; half < D / 64; ++half) {
-                            tma_load_2d(kd + half * kPage * 128, &tm_k, &full[stg], half * 64, row0, kEvictFirst);
-                            tma_load_2d(vd + half * kPage * 128, &tm_v, &full[stg], half * 64, row0, kEvictFirst);
+                    for (int k = 0; k < (NCW * kPage) / 32; ++k) {
+                        const int rr = lane + 32 * k, w = rr / kPage, r = rr % kPage;
+                        const int lp_w = __shfl_sync(0xffffffffu, my_lp, j + w);
+                        int t = -1;
+                        if (w < valid) {
+                            t = lp_w * kPage + r;
+                            if (t >= s) t = -1;
                         }
+                        rowtok[(stg * NCW + w) * kPage + r] = t;
+                    }
+                    const int phys_w = __shfl_sync(0xffffffffu, my_phys, j + (lane % NCW));
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_expect_tx(&full[stg], valid * C::kTile);
+                    __syncwarp();
+                    if (lane < valid) {  // one 2P-row box: this head's K and V rows of the page
+                        const int row0 = (int)kv_row(layer_ph + phys_w, p.g, h, 0);
+                        uint8_t* dst = ring + (stg * NCW + lane) * C::kTile;
+                        if (D == 64) tma_load_2d(dst, &tm_kv, &full[stg], 0, row0, kEvictFirst);
+                        else tma_load_3d(dst, &tm_kv, &full[stg], 0, 0, row0, kEvictFirst);
                     }
                 }
             }
         } else {
-            const __nv_bfloat16* kp = reinterpret_cast<const __nv_bfloat16*>(p.k_pool);
-            const __nv_bfloat16* vp = reinterpret_cast<const __nv_bfloat16*>(p.v_pool);
+            const __nv_bfloat16* pool = reinterpret_cast<const __nv_bfloat16*>(p.kv_pool);
             constexpr int kChunks = D / 8;
+            constexpr int kRowsPerStage = NCW * kPage;  // 64
             for (int it = 0, iter = 0; it < n_items; it += NCW, ++iter) {
                 const int stg = iter % NSTAGE, round = iter / NSTAGE;
+                // resolve the stage's rows: lane owns rows lane and lane + 32 (token -> pool row)
+                long long my_row[kRowsPerStage / 32];
+                int my_t[kRowsPerStage / 32];
+#pragma unroll
+                for (int k = 0; k < kRowsPerStage / 32; ++k) {  // token and its physical slot: independent
+                    const int rr = lane + 32 * k, w = rr / kPage, r = rr % kPage;
+                    const int e = unit0 + (it + w) * kPage + r;
+                    const bool ok = it + w < n_items && e < e_end;
+                    my_t[k] = ok ? plan[e] : -1;
+                    const int ps = ok ? plan_phys[e] : 0;  // phys_page * P + slot
+                    my_row[k] = ok ? (long long)kv_row(layer_ph + ps / kPage, p.g, h, ps % kPage) : -1ll;
+                }
                 if (round > 0) mbar_wait(&empty[stg], (round - 1) & 1);
+#pragma unroll
+                for (int k = 0; k < kRowsPerStage / 32; ++k) rowtok[stg * kRowsPerStage + lane + 32 * k] = my_t[k];
                 for (int w = 0; w < NCW; ++w) {
-                    const int item = it + w;
-                    if (item >= n_items) break;
-                    // lane r < 16 resolves row r of this tile: token -> pool row
-                    long long my_row = -1;
-                    if (lane < 16) {
-                        const int e = unit0 + item * 16 + lane;
-                        if (e < e_end) {
-                            const int t = plan[e];
-                            my_row = (long long)(((layer_ph + bt[t / kPage]) * p.g + h) * kPage + (t % kPage));
-                        }
-                    }
-                    uint8_t* kd = kbuf + (stg * NCW + w) * C::kTile;
-                    uint8_t* vd = vbuf + (stg * NCW + w) * C::kTile;
-                    for (int ci = lane; ci < 16 * kChunks; ci += 32) {
+                    if (it + w >= n_items) break;
+                    uint8_t* kd = ring + (stg * NCW + w) * C::kTile;
+                    uint8_t* vd = kd + C::kHalf;
+                    for (int ci = lane; ci < kPage * kChunks; ci += 32) {
                         const int r = ci / kChunks, c = ci - r * kChunks;
-                        const long long row = __shfl_sync(0xffffffffu, my_row, r);
+                        const int rr = w * kPage + r;
+                        const long long r0 = __shfl_sync(0xffffffffu, my_row[0], rr & 31);
+                        const long long r1 = __shfl_sync(0xffffffffu, my_row[1], rr & 31);
+                        const long long row = (rr >> 5) ? r1 : r0;
                         if (row >= 0) {
-                            cp_async16(kd + swz(r, c), kp + row * D + c * 8);
-                            cp_async16(vd + swz(r, c), vp + row * D + c * 8);
+                            cp_async16(kd + swz<D>(r, c), pool + row * D + c * 8);
+                            cp_async16(vd + swz<D>(r, c), pool + (row + kPage) * D + c * 8);
                         }
                     }
                 }
@@ -170,49 +241,54 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__
         }
     } else {
         // ============================================================ consumers
+        // "Swapped" GQA tile: tokens are the MMA M dimension and the group's query heads the
+        // N dimension (NH tiles of 8), so no MMA row is spent on padding heads:
+        //   S^T[16 tok x 8 heads] = K[16 x D] . Q^T[D x 8]          (D/16 MMAs)
+        //   O^T[D x 8 heads]     += V^T[D x 16 tok] . P^T[16 x 8]   (2 x D/16 MMAs: P hi + lo)
+        // The S^T accumulator becomes the P^T operand with two movmatrix transposes per half.
+        // Lane (g4 = lane/4, t4 = lane%4) owns heads 2*t4, 2*t4+1 of each head tile, tokens g4
+        // and g4+8 of S^T, and rows d = 16*mt + g4 (+8) of O^T.
+        // NH = head tiles of 8 (1: gs <= 8, 2: gs <= 16); tiles past gs are skipped
         const int g4 = lane >> 2, t4 = lane & 3;
         const int gs = p.gs;
-        // Q fragments (A operand, rows = query heads of the group, zero-padded to 16)
-        uint32_t qa[D / 16][4];
+        const int nh_used = (gs + 7) / 8;
+        // Q^T fragments (B operand): qb[nh][kc] = Q[head nh*8+g4][16kc + 2t4 (+1)], [.. + 8 (+9)]
+        uint32_t qb[NH][D / 16][2];
         {
             const __nv_bfloat16* qp = reinterpret_cast<const __nv_bfloat16*>(p.q) + ((size_t)b * p.m + h * gs) * D;
-            const uint32_t* q0 = reinterpret_cast<const uint32_t*>(qp + (size_t)g4 * D);
-            const uint32_t* q1 = reinterpret_cast<const uint32_t*>(qp + (size_t)(g4 + 8) * D);
-            const bool v0 = g4 < gs, v1 = g4 + 8 < gs;
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-                const int c = (kk * 16 + t4 * 2) >> 1;
-                qa[kk][0] = v0 ? q0[c] : 0u;
-                qa[kk][1] = v1 ? q1[c] : 0u;
-                qa[kk][2] = v0 ? q0[c + 4] : 0u;
-                qa[kk][3] = v1 ? q1[c + 4] : 0u;
+            for (int nh = 0; nh < NH; ++nh) {
+                const int hq = nh * 8 + g4;
+                const uint32_t* qr = reinterpret_cast<const uint32_t*>(qp + (size_t)hq * D);
+#pragma unroll
+                for (int kc = 0; kc < D / 16; ++kc) {
+                    qb[nh][kc][0] = hq < gs ? qr[(kc * 16 + 2 * t4) >> 1] : 0u;
+                    qb[nh][kc][1] = hq < gs ? qr[(kc * 16 + 2 * t4 + 8) >> 1] : 0u;
+                }
             }
         }
-        float o[D / 8][4];
+        float o[NH][D / 16][4];
+        float mh[NH][2], lh[NH][2];
 #pragma unroll
-        for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+        for (int nh = 0; nh < NH; ++nh) {
+            mh[nh][0] = mh[nh][1] = -INFINITY;
+            lh[nh][0] = lh[nh][1] = 0.f;
+#pragma unroll
+            for (int mt = 0; mt < D / 16; ++mt) o[nh][mt][0] = o[nh][mt][1] = o[nh][mt][2] = o[nh][mt][3] = 0.f;
+        }
         const float sl2 = p.scale_log2;
 
         for (int it = 0, iter = 0; it < n_items; it += NCW, ++iter) {
             const int stg = iter % NSTAGE, round = iter / NSTAGE;
             mbar_wait(&full[stg], round & 1);
+            if (iter == 0 && tid == 0) DTRACE(2);
             const int item = it + warp;
             if (item < n_items) {
-                uint8_t* kt = kbuf + (stg * NCW + warp) * C::kTile;
-                uint8_t* vt = vbuf + (stg * NCW + warp) * C::kTile;
-                // token of row `lane` (lanes 0..15); -1 = no token
-                int my_tok = -1;
-                if (lane < 16) {
-                    if (!TOKEN_PLAN) {
-                        const int lp = (p.role == kRoleSparse) ? plan[unit0 + item] : unit0 + item;
-                        const int t = lp * kPage + lane;
-                        my_tok = (t < s) ? t : -1;
-                    } else {
-                        const int e = unit0 + item * 16 + lane;
-                        my_tok = (e < e_end) ? plan[e] : -1;
-                    }
-                }
+                uint8_t* kt = ring + (stg * NCW + warp) * C::kTile;
+                uint8_t* vt = kt + C::kHalf;
+                const int* rt = rowtok + (stg * NCW + warp) * kPage;
+                const int my_tok = (lane < kPage) ? rt[lane] : -1;  // token of ring row `lane`
+                const int tok0 = rt[g4], tok1 = rt[g4 + 8];         // tokens of this lane's S^T rows
                 // fused append: patch row holding token s-1 from the inputs
                 if (p.fuse_append) {
                     const unsigned pm = __ballot_sync(0xffffffffu, my_tok == s - 1);
@@ -220,9 +296,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__
                         const int r = __ffs(pm) - 1;
                         constexpr int kChunks = D / 8;
                         if (lane < kChunks)
-                            *reinterpret_cast<uint4*>(kt + swz(r, lane)) = reinterpret_cast<const uint4*>(k_new)[lane];
+                            *reinterpret_cast<uint4*>(kt + swz<D>(r, lane)) = reinterpret_cast<const uint4*>(k_new)[lane];
                         else if (lane < 2 * kChunks)
-                            *reinterpret_cast<uint4*>(vt + swz(r, lane - kChunks)) =
+                            *reinterpret_cast<uint4*>(vt + swz<D>(r, lane - kChunks)) =
                                 reinterpret_cast<const uint4*>(v_new)[lane - kChunks];
                     }
                 }
@@ -234,93 +310,92 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__
                     while (inval) {
                         const int r = __ffs(inval) - 1;
                         inval &= inval - 1;
-                        if (lane < D / 8) *reinterpret_cast<uint4*>(vt + swz(r, lane)) = make_uint4(0, 0, 0, 0);
+                        if (lane < D / 8) *reinterpret_cast<uint4*>(vt + swz<D>(r, lane)) = make_uint4(0, 0, 0, 0);
                     }
                 }
                 __syncwarp();
-                // ---- S = Q K^T (16 q rows x 16 tokens)
-                float acc[2][4];
                 const uint32_t kt_u = smem_u32(kt), vt_u = smem_u32(vt);
+                // ---- S^T = K Q^T: two accumulator chains (even / odd k-chunks)
+                float acc[NH][4], acc2[NH][4];
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt) {
-                    acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+                for (int nh = 0; nh < NH; ++nh)
 #pragma unroll
-                    for (int kc = 0; kc < D / 32; ++kc) {
-                        uint32_t b0, b1, b2, b3;
-                        ldsm_x4(kt_u + swz(nt * 8 + (lane & 7), kc * 4 + (lane >> 3)), b0, b1, b2, b3);
-                        mma_bf16_16816(acc[nt], qa[2 * kc], b0, b1);
-                        mma_bf16_16816(acc[nt], qa[2 * kc + 1], b2, b3);
+                    for (int i = 0; i < 4; ++i) acc[nh][i] = acc2[nh][i] = 0.f;
+#pragma unroll
+                for (int kc = 0; kc < D / 16; ++kc) {
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4(kt_u + swz<D>((lane & 7) + 8 * ((lane >> 3) & 1), kc * 2 + (lane >> 4)), a0, a1, a2, a3);
+                    const uint32_t af[4] = {a0, a1, a2, a3};
+#pragma unroll
+                    for (int nh = 0; nh < NH; ++nh) {
+                        if (nh < nh_used) {
+                            if (kc & 1) mma_bf16_16816(acc2[nh], af, qb[nh][kc][0], qb[nh][kc][1]);
+                            else mma_bf16_16816(acc[nh], af, qb[nh][kc][0], qb[nh][kc][1]);
+                        }
                     }
                 }
-                // tokens of this lane's accumulator columns: col = nt*8 + 2*t4 + (i&1)
-                int tk[2][2];
+                uint32_t bhi[NH][2], blo[NH][2];
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt)
+                for (int nh = 0; nh < NH; ++nh) {
+                    if (nh >= nh_used) continue;
+                    float c[4];
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) tk[nt][e] = __shfl_sync(0xffffffffu, my_tok, nt * 8 + 2 * t4 + e);
-                if (p.role == kRoleSelect) {
-                    float* lg = p.logits + (size_t)b * p.max_seq * p.m + h * gs;
-#pragma unroll
-                    for (int nt = 0; nt < 2; ++nt)
+                    for (int i = 0; i < 4; ++i) c[i] = acc[nh][i] + acc2[nh][i];
+                    // c[0],c[1]: token tok0, heads 2t4, 2t4+1; c[2],c[3]: token tok1
+                    if (p.role == kRoleSelect) {
+                        float* lg = p.logits + (size_t)b * p.max_seq * p.m + h * gs;
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
-                            const int row = (i < 2) ? g4 : g4 + 8;
-                            const int t = tk[nt][i & 1];
-                            if (row < gs && t >= 0) lg[(size_t)t * p.m + row] = acc[nt][i] * p.scale;
+                            const int hq = nh * 8 + 2 * t4 + (i & 1);
+                            const int t = (i < 2) ? tok0 : tok1;
+                            if (hq < gs && t >= 0) lg[(size_t)t * p.m + hq] = c[i] * p.scale;
                         }
-                }
-                // ---- online softmax (log2 domain)
-                float x[2][4];
-#pragma unroll
-                for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) x[nt][i] = (tk[nt][i & 1] >= 0) ? acc[nt][i] * sl2 : -INFINITY;
-                float mx0 = fmaxf(fmaxf(x[0][0], x[0][1]), fmaxf(x[1][0], x[1][1]));
-                float mx1 = fmaxf(fmaxf(x[0][2], x[0][3]), fmaxf(x[1][2], x[1][3]));
-                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-                const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-                const float ms0 = (mn0 == -INFINITY) ? 0.f : mn0;
-                const float ms1 = (mn1 == -INFINITY) ? 0.f : mn1;
-                const float a0 = ex2(m0 - ms0), a1 = ex2(m1 - ms1);
-                float pr[2][4];
-#pragma unroll
-                for (int nt = 0; nt < 2; ++nt) {
-                    pr[nt][0] = ex2(x[nt][0] - ms0);
-                    pr[nt][1] = ex2(x[nt][1] - ms0);
-                    pr[nt][2] = ex2(x[nt][2] - ms1);
-                    pr[nt][3] = ex2(x[nt][3] - ms1);
-                }
-                l0 = l0 * a0 + (pr[0][0] + pr[0][1] + pr[1][0] + pr[1][1]);
-                l1 = l1 * a1 + (pr[0][2] + pr[0][3] + pr[1][2] + pr[1][3]);
-                m0 = mn0;
-                m1 = mn1;
-#pragma unroll
-                for (int n = 0; n < D / 8; ++n) {
-                    o[n][0] *= a0; o[n][1] *= a0; o[n][2] *= a1; o[n][3] *= a1;
-                }
-                // ---- O += P V, P split into bf16 hi + lo
-                uint32_t ahi[4], alo[4];
-                {
-                    const float* f[4] = {&pr[0][0], &pr[0][2], &pr[1][0], &pr[1][2]};
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const __nv_bfloat162 hv = __floats2bfloat162_rn(f[i][0], f[i][1]);
-                        const float2 hf = __bfloat1622float2(hv);
-                        ahi[i] = *reinterpret_cast<const uint32_t*>(&hv);
-                        alo[i] = pack_bf16(f[i][0] - hf.x, f[i][1] - hf.y);
                     }
-                }
+                    // ---- online softmax per head column (log2 domain)
+                    float pr[4];
 #pragma unroll
-                for (int vc = 0; vc < D / 16; ++vc) {
-                    uint32_t b0, b1, b2, b3;
-                    ldsm_x4_t(vt_u + swz(((lane >> 3) & 1) * 8 + (lane & 7), vc * 2 + (lane >> 4)), b0, b1, b2, b3);
-                    mma_bf16_16816(o[2 * vc], ahi, b0, b1);
-                    mma_bf16_16816(o[2 * vc], alo, b0, b1);
-                    mma_bf16_16816(o[2 * vc + 1], ahi, b2, b3);
-                    mma_bf16_16816(o[2 * vc + 1], alo, b2, b3);
+                    for (int e = 0; e < 2; ++e) {
+                        const float x0 = tok0 >= 0 ? c[e] * sl2 : -INFINITY;
+                        const float x1 = tok1 >= 0 ? c[2 + e] * sl2 : -INFINITY;
+                        float mx = fmaxf(x0, x1);
+                        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+                        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+                        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+                        const float mn = fmaxf(mh[nh][e], mx);
+                        const float msafe = (mn == -INFINITY) ? 0.f : mn;
+                        const float al = ex2(mh[nh][e] - msafe);
+                        pr[e] = ex2(x0 - msafe);
+                        pr[2 + e] = ex2(x1 - msafe);
+                        lh[nh][e] = lh[nh][e] * al + (pr[e] + pr[2 + e]);
+                        mh[nh][e] = mn;
+#pragma unroll
+                        for (int mt = 0; mt < D / 16; ++mt) {
+                            o[nh][mt][e] *= al;
+                            o[nh][mt][2 + e] *= al;
+                        }
+                    }
+                    // ---- P^T operand: bf16 hi + lo (P keeps ~16 mantissa bits), transposed
+                    const __nv_bfloat162 h01 = __floats2bfloat162_rn(pr[0], pr[1]);
+                    const __nv_bfloat162 h23 = __floats2bfloat162_rn(pr[2], pr[3]);
+                    const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+                    bhi[nh][0] = movmatrix_trans(*reinterpret_cast<const uint32_t*>(&h01));
+                    bhi[nh][1] = movmatrix_trans(*reinterpret_cast<const uint32_t*>(&h23));
+                    blo[nh][0] = movmatrix_trans(pack_bf16(pr[0] - f01.x, pr[1] - f01.y));
+                    blo[nh][1] = movmatrix_trans(pack_bf16(pr[2] - f23.x, pr[3] - f23.y));
+                }
+                // ---- O^T += V^T P^T
+#pragma unroll
+                for (int mt = 0; mt < D / 16; ++mt) {
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4_t(vt_u + swz<D>((lane & 7) + 8 * (lane >> 4), mt * 2 + ((lane >> 3) & 1)), a0, a1, a2, a3);
+                    const uint32_t af[4] = {a0, a1, a2, a3};
+#pragma unroll
+                    for (int nh = 0; nh < NH; ++nh) {
+                        if (nh < nh_used) {
+                            mma_bf16_16816(o[nh][mt], af, bhi[nh][0], bhi[nh][1]);
+                            mma_bf16_16816(o[nh][mt], af, blo[nh][0], blo[nh][1]);
+                        }
+                    }
                 }
                 // generic-proxy smem writes must be ordered before the next TMA refill
                 if (wrote_smem) fence_proxy_async_smem();
@@ -328,71 +403,113 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stg]);
         }
-        // quad-reduce the row sums
-        l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-        l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-        l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-        l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
 
-        // ---------------------------------------------------------------- merge
+        // ---------------------------------------------------------------- warp states
+        if (tid == 0) DTRACE(3);
         consumer_bar(NCW * 32);  // every consumer is done reading the ring
-        float* ms = reinterpret_cast<float*>(kbuf);
-        float* ls = ms + NCW * 16;
-        float* os = ls + NCW * 16;
-        if (t4 == 0) {
-            ms[warp * 16 + g4] = m0; ls[warp * 16 + g4] = l0;
-            ms[warp * 16 + g4 + 8] = m1; ls[warp * 16 + g4 + 8] = l1;
-        }
 #pragma unroll
-        for (int n = 0; n < D / 8; ++n) {
-            const int col = n * 8 + 2 * t4;
-            if (g4 < gs) {
-                os[(warp * 16 + g4) * D + col] = o[n][0];
-                os[(warp * 16 + g4) * D + col + 1] = o[n][1];
+        for (int nh = 0; nh < NH; ++nh) {
+            if (nh >= nh_used) continue;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                float l = lh[nh][e];  // column sum over the 8 token-row groups
+                l += __shfl_xor_sync(0xffffffffu, l, 4);
+                l += __shfl_xor_sync(0xffffffffu, l, 8);
+                l += __shfl_xor_sync(0xffffffffu, l, 16);
+                const int hq = nh * 8 + 2 * t4 + e;
+                if (g4 == 0 && hq < gs) {
+                    ms[warp * 16 + hq] = mh[nh][e];
+                    ls[warp * 16 + hq] = l;
+                }
             }
-            if (g4 + 8 < gs) {
-                os[(warp * 16 + g4 + 8) * D + col] = o[n][2];
-                os[(warp * 16 + g4 + 8) * D + col + 1] = o[n][3];
-            }
+#pragma unroll
+            for (int mt = 0; mt < D / 16; ++mt)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int hq = nh * 8 + 2 * t4 + (i & 1);
+                    const int dd = mt * 16 + g4 + 8 * (i >> 1);
+                    if (hq < gs) os[(warp * 16 + hq) * os_stride<D>() + dd] = o[nh][mt][i];
+                }
         }
-        consumer_bar(NCW * 32);
-        pdl_launch_dependents();
-        cta_merge<D>(p, ms, ls, os, NCW, b, h, split, tid, NCW * 32);
-        grid_combine<D>(p, b, h, s, stale, cap_err, tid, NCW * 32, sflag);
     }
+    __syncthreads();  // producer joins: warp states complete
+    pdl_launch_dependents();
+    if (tid == 0) DTRACE(4);
+    cluster_epilogue<D, NCW>(p, ms, ls, os, cstage, b, h, stale, cap_err, s);
+    if (tid == 0) DTRACE(6);
 }
 
-template <int D, bool TOKEN_PLAN>
-cudaError_t launch_impl(const AttnParams& p, const CUtensorMap* tm_k, const CUtensorMap* tm_v,
+template <int D, bool TOKEN_PLAN, int NST, int NH>
+cudaError_t launch_impl(const AttnParams& p0, const CUtensorMap* tm_kv,
                         cudaStream_t st, bool pdl) {
-    auto kern = attn_tc_kernel<D, TOKEN_PLAN>;
-    constexpr int smem = TcCfg<D>::kSmem;
-    static bool configured = false;
-    if (!configured) {
+    auto kern = attn_tc_kernel<D, TOKEN_PLAN, NST, NH>;
+    constexpr int smem = TcCfg<D, NST>::kSmem;
+    static int max_cluster = 0;  // largest feasible cluster for this instantiation
+    if (max_cluster == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
-        configured = true;
+        max_cluster = cluster_limit((const void*)kern, kThreads, smem);
     }
+    AttnParams p = p0;
+    p.nsplit = std::min(p.nsplit, max_cluster);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.nsplit, p.g, p.batch);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.nsplit;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, *tm_k, *tm_v, p);
+    cfg.numAttrs = pdl ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, *tm_kv, p);
+}
+
+template <int D, bool TOKEN_PLAN>
+cudaError_t launch_stages(const AttnParams& p, const CUtensorMap* tm_kv, cudaStream_t st,
+                          bool pdl) {
+    if (p.gs <= 8)
+        return p.deep ? launch_impl<D, TOKEN_PLAN, kDeep, 1>(p, tm_kv, st, pdl)
+                      : launch_impl<D, TOKEN_PLAN, kShallow, 1>(p, tm_kv, st, pdl);
+    return p.deep ? launch_impl<D, TOKEN_PLAN, kDeep, 2>(p, tm_kv, st, pdl)
+                  : launch_impl<D, TOKEN_PLAN, kShallow, 2>(p, tm_kv, st, pdl);
 }
 
 }  // namespace
 
-cudaError_t launch_attn_tc(const AttnParams& p, const CUtensorMap* tm_k, const CUtensorMap* tm_v,
+#ifdef DELTA_TRACE
+// trace builds: max co-resident clusters of the real kernel for a cluster size
+extern "C" int delta_debug_cluster_occupancy(int deep, int cs) {
+    auto kern = deep ? attn_tc_kernel<128, false, kDeep, 1> : attn_tc_kernel<128, false, kShallow, 1>;
+    const int smem = deep ? TcCfg<128, kDeep>::kSmem : TcCfg<128, kShallow>::kSmem;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs, 8, 1);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute a;
+    a.id = cudaLaunchAttributeClusterDimension;
+    a.val.clusterDim.x = cs; a.val.clusterDim.y = 1; a.val.clusterDim.z = 1;
+    cfg.attrs = &a; cfg.numAttrs = 1;
+    int n = -1;
+    if (cudaOccupancyMaxActiveClusters(&n, (const void*)kern, &cfg) != cudaSuccess) { cudaGetLastError(); return -2; }
+    return n;
+}
+#endif
+
+cudaError_t launch_attn_tc(const AttnParams& p, const CUtensorMap* tm_kv,
                            cudaStream_t st, bool pdl) {
     const bool tok = (p.role == kRoleSparse) && p.sel_block == 1;
-    if (p.d == 128) return tok ? launch_impl<128, true>(p, tm_k, tm_v, st, pdl) : launch_impl<128, false>(p, tm_k, tm_v, st, pdl);
-    if (p.d == 64) return tok ? launch_impl<64, true>(p, tm_k, tm_v, st, pdl) : launch_impl<64, false>(p, tm_k, tm_v, st, pdl);
+    if (p.d == 128)
+        return tok ? launch_stages<128, true>(p, tm_kv, st, pdl) : launch_stages<128, false>(p, tm_kv, st, pdl);
+    if (p.d == 64)
+        return tok ? launch_stages<64, true>(p, tm_kv, st, pdl) : launch_stages<64, false>(p, tm_kv, st, pdl);
     return cudaErrorInvalidValue;
 }
 

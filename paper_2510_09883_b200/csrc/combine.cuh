@@ -1,21 +1,32 @@
-// combine.cuh — split-K (flash-decoding) merge used by every attention kernel.
+// combine.cuh — split-K (flash-decoding) merge used by every attention kernel, done inside
+// a thread-block cluster through distributed shared memory (no global partials, no
+// arrival counters, no grid-wide fences).
 //
 // Within a CTA, each warp keeps an online-softmax state (running max m in log2 units,
-// running sum l, unnormalised O) over the tokens it processed.  cta_merge() folds the
-// warps' states (fixed warp order) into ONE partial (o normalised, lse in log2 units)
-// per (sequence, kv head, split, query head).  grid_combine() then elects the last CTA
-// of each (sequence, kv head) with an arrival counter ("last block done"), which merges
-// all splits in ascending split order — a fixed order, so results are deterministic —
-// and writes O, LSE.  This is the identity LSE = log sum_s exp(lse_s),
-// O = sum_s exp(lse_s - LSE) o_s (any partition of the token set gives the same
-// attention, Eq.4).
+// running sum l, unnormalised O) over the tokens it processed.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "internal.h"
 #include "ptx.cuh"
 
 namespace delta {
 
 constexpr float kLn2 = 0.6931471805599453f;
+
+// Dedicated shared-memory staging that cluster peers push into (must not overlap anything
+// the owning CTA still uses while peers may be writing, e.g. its TMA ring).
+template <int D>
+struct ClusterStage {
+    static constexpr int kO4 = 16 * D / 4 + kMaxSplit;            // float4 slots: sO[rank * per + k]
+    static constexpr int kFloats = kO4 * 4 + 2 * kMaxSplit * 16;  // + sM[rank][16], sL[rank][16]
+    static constexpr int kBytes = kFloats * 4;
+};
+
+// Row stride (floats) of the per-warp O states: D + 4 makes the fragment-order stores of
+// the MMA accumulators bank-conflict free and keeps float4 rows aligned.
+template <int D>
+constexpr int os_stride() { return D + 4; }
 
 __device__ __forceinline__ void consumer_bar(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
@@ -25,88 +36,128 @@ __device__ __forceinline__ void set_err(int32_t* err, int code) {
     if (err) atomicCAS(err, 0, code);
 }
 
-// smem layout for the per-warp states: ms[NW][16], ls[NW][16], os[NW][16][D]
-template <int D>
-__device__ __forceinline__ void cta_merge(const AttnParams& p, const float* ms, const float* ls,
-                                          const float* os, int nw, int b, int h, int split,
-                                          int tid, int nthreads) {
+// Cluster split-K epilogue, called by EVERY thread of every CTA of the cluster (the
+// cluster = the `nsplit` CTAs of one (sequence, kv head); rank = split).  Push model, one
+// cluster barrier:
+//  1. each thread folds the warps' states (ms[w*16+row] running max in log2 units, ls
+//     running sum, os[(w*16+row)*OS+col] unnormalised O) in fixed warp order into this CTA's
+//     (M_c, L_c, O_c) for its float4 of the gs x D output, and stores it straight into the
+//     shared staging of the CTA that owns that output slice (distributed shared memory);
+//  2. cluster barrier (release / acquire): every pushed value is visible to its owner;
+//  3. the owner of a slice merges the ns partials from its own shared memory in ascending
+//     rank order: M = max_c M_c, w_c = exp2(M_c - M), L = sum_c w_c L_c,
+//     O = sum_c w_c O_c / L, LSE = (M + log2 L) ln 2 — the identity that any partition of
+//     the attended token set gives the same softmax (Eq.4).  Fixed order:
+//     deterministic.  No CTA touches a peer's memory after the barrier.
+//  Rank 0 then reports device errors and, for a fused append, adds 1 to the length counter.
+//
+// Length counter encoding: seq_len_raw[l][b] = n * g.  Each of the g head clusters of a
+// fused append+decode adds 1 when it is done; every reader takes raw / g, which is exact
+// because a reader's own cluster has not yet added, so at most g - 1 additions precede it.
+template <int D, int NW>
+__device__ __forceinline__ void cluster_epilogue(const AttnParams& p, const float* ms, const float* ls,
+                                                 const float* os, float* stage, int b, int h, bool stale,
+                                                 bool cap_err, int s_post) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int tid = threadIdx.x, nthreads = blockDim.x;
     const int gs = p.gs;
-    for (int idx = tid; idx < gs * D; idx += nthreads) {
-        const int row = idx / D, col = idx - row * D;
-        float M = -INFINITY;
-        for (int w = 0; w < nw; ++w) M = fmaxf(M, ms[w * 16 + row]);
-        float L = 0.f, o = 0.f;
-        if (M != -INFINITY) {
-            for (int w = 0; w < nw; ++w) {
-                const float mw = ms[w * 16 + row];
-                const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
-                L += ls[w * 16 + row] * f;
-                o += os[(w * 16 + row) * D + col] * f;
+    const int ns = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+    constexpr int C4 = D / 4, OS = os_stride<D>();
+    const int total = gs * C4;
+    const int per = (total + ns - 1) / ns;
+    float4* sO = reinterpret_cast<float4*>(stage);
+    float* sM = stage + ClusterStage<D>::kO4 * 4;
+    float* sL = sM + kMaxSplit * 16;
+    // 1. push: each thread folds the NW warp states of one float4 (fixed warp order, fully
+    //    unrolled so every shared load is in flight at once) and stores it into the owner's
+    //    staging; the c4 == 0 thread of a row also pushes the row's (M_c, L_c) to every owner.
+    for (int idx = tid; idx < total; idx += nthreads) {
+        const int row = idx / C4, c4 = idx - row * C4;
+        float mw[NW];
+        float4 v[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            mw[w] = ms[w * 16 + row];
+            v[w] = reinterpret_cast<const float4*>(os + (w * 16 + row) * OS)[c4];
+        }
+        float M = mw[0];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) M = fmaxf(M, mw[w]);
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        float f[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            f[w] = (M == -INFINITY || mw[w] == -INFINITY) ? 0.f : exp2f(mw[w] - M);
+            o.x += f[w] * v[w].x; o.y += f[w] * v[w].y; o.z += f[w] * v[w].z; o.w += f[w] * v[w].w;
+        }
+        const int r = idx / per, k = idx - r * per;
+        cl.map_shared_rank(sO, r)[rank * per + k] = o;
+        if (c4 == 0) {
+            float L = 0.f;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) L += ls[w * 16 + row] * f[w];
+            for (int rr = 0; rr < ns; ++rr) {
+                cl.map_shared_rank(sM, rr)[rank * 16 + row] = M;
+                cl.map_shared_rank(sL, rr)[rank * 16 + row] = L;
             }
         }
-        const size_t prow = ((size_t)(b * p.g + h) * p.nsplit + split) * gs + row;
-        p.part_o[prow * D + col] = (L > 0.f) ? o / L : 0.f;
-        if (col == 0) p.part_lse[prow] = (L > 0.f) ? M + log2f(L) : -INFINITY;
     }
-}
-
-// Called by `nthreads` threads (named barrier 1) after cta_merge.  s_post: cache length
-// after this launch (used to bump seq_len when the launch fused the append).
-template <int D>
-__device__ __forceinline__ void grid_combine(const AttnParams& p, int b, int h, int s_post, bool stale,
-                                             bool capacity_err, int tid, int nthreads, int* sflag) {
-    __threadfence();
-    consumer_bar(nthreads);
-    if (tid == 0) {
-        const int t = atomicAdd(&p.cnt_head[b * p.g + h], 1);
-        *sflag = (t == p.nsplit - 1);
-    }
-    consumer_bar(nthreads);
-    if (!*sflag) return;
-    __threadfence();
-    const int gs = p.gs;
-    const size_t base = (size_t)(b * p.g + h) * p.nsplit;
+    if (tid == 0) DTRACE(5);
+    cl.sync();  // release / acquire: every pushed value is visible to its owner
+    if (tid == 0) DTRACE(7);
+    // 2. owner: 16 lanes per owned float4, lane c holds rank c's partial; max, weights and
+    //    sums are fixed shuffle trees over the 16 lanes (deterministic).
     bool bad = false;
-    for (int idx = tid; idx < gs * D; idx += nthreads) {
-        const int row = idx / D, col = idx - row * D;
-        float M = -INFINITY;
-        for (int sp = 0; sp < p.nsplit; ++sp) M = fmaxf(M, __ldcg(&p.part_lse[(base + sp) * gs + row]));
-        float L2 = -INFINITY, o = 0.f;
-        if (M != -INFINITY) {
-            float W = 0.f;
-            for (int sp = 0; sp < p.nsplit; ++sp) {
-                const float l = __ldcg(&p.part_lse[(base + sp) * gs + row]);
-                if (l != -INFINITY) W += exp2f(l - M);
-            }
-            L2 = M + log2f(W);
-            for (int sp = 0; sp < p.nsplit; ++sp) {
-                const float l = __ldcg(&p.part_lse[(base + sp) * gs + row]);
-                if (l != -INFINITY) o += exp2f(l - L2) * __ldcg(&p.part_o[((base + sp) * gs + row) * D + col]);
-            }
+    const int grp = tid >> 4, c = tid & 15, ngrp = nthreads >> 4;
+    for (int k0 = 0; k0 < per; k0 += ngrp) {
+        const int k = k0 + grp;
+        const int idx = rank * per + k;
+        const bool live = k < per && idx < total;
+        const int row = live ? idx / C4 : 0, c4 = live ? idx - row * C4 : 0;
+        const bool mine = live && c < ns;
+        float mc = mine ? sM[c * 16 + row] : -INFINITY;
+        float lc = mine ? sL[c * 16 + row] : 0.f;
+        float4 x = mine ? sO[c * per + k] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float M = mc;
+#pragma unroll
+        for (int off = 8; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+        const float f = (M == -INFINITY || mc == -INFINITY) ? 0.f : exp2f(mc - M);
+        float L = f * lc;
+        float4 v = make_float4(f * x.x, f * x.y, f * x.z, f * x.w);
+#pragma unroll
+        for (int off = 8; off > 0; off >>= 1) {
+            L += __shfl_xor_sync(0xffffffffu, L, off);
+            v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+            v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+            v.z += __shfl_xor_sync(0xffffffffu, v.z, off);
+            v.w += __shfl_xor_sync(0xffffffffu, v.w, off);
         }
-        if (stale) o = __int_as_float(0x7fc00000);  // NaN: stale plan must be loud
-        else if (!isfinite(o)) bad = true;
-        const int j = h * gs + row;
-        p.out[((size_t)b * p.m + j) * D + col] = o;
-        if (col == 0) {
-            const float lse = (L2 == -INFINITY) ? -INFINITY : L2 * kLn2;
-            if (p.lse_out) p.lse_out[(size_t)b * p.m + j] = lse;
-            if (p.role == kRoleSelect) p.lse_buf[(size_t)b * p.m + j] = lse;
+        if (live && c == 0) {
+            const float inv = (L > 0.f) ? 1.f / L : 0.f;
+            float4 o = make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv);
+            if (stale) {
+                const float qn = __int_as_float(0x7fc00000);  // NaN: stale plan must be loud
+                o = make_float4(qn, qn, qn, qn);
+            } else if (!(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w))) {
+                bad = true;
+            }
+            const int j = h * gs + row;
+            reinterpret_cast<float4*>(p.out + ((size_t)b * p.m + j) * D)[c4] = o;
+            if (c4 == 0) {
+                const float lse = (L > 0.f) ? (M + log2f(L)) * kLn2 : -INFINITY;
+                if (p.lse_out) p.lse_out[(size_t)b * p.m + j] = lse;
+                if (p.role == kRoleSelect) p.lse_buf[(size_t)b * p.m + j] = lse;
+            }
         }
     }
+    if (tid == 0) DTRACE(9);
     if (bad) set_err(p.err, kDevNumeric);
-    consumer_bar(nthreads);
-    if (tid == 0) {
+    if (rank == 0 && tid == 0) {
         if (stale) set_err(p.err, kDevUsage);
-        if (capacity_err) set_err(p.err, kDevCapacity);
+        if (cap_err) set_err(p.err, kDevCapacity);
         if (s_post <= 0) set_err(p.err, kDevUsage);  // attention over an empty cache
-        p.cnt_head[b * p.g + h] = 0;
-        __threadfence();
-        const int t2 = atomicAdd(&p.cnt_seq[b], 1);
-        if (t2 == p.g - 1) {
-            if (p.fuse_append && !capacity_err) p.seq_len[p.layer * p.max_batch + b] = s_post;
-            p.cnt_seq[b] = 0;
-        }
+        if (p.fuse_append && !cap_err) atomicAdd(&p.seq_len[p.layer * p.max_batch + b], 1);
     }
 }
 

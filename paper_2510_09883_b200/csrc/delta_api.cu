@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -25,9 +26,9 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
-    size_t seq_len, err, cnt_head, cnt_seq, cnt_sel, part_o, part_lse, logits, lse_buf, keys,
-        plan_idx, plan_count, plan_stamp, stage_q, stage_k, stage_v, stage_out, total;
-    int rows_max, max_units, plan_cap, n_delta, max_pages;
+    size_t seq_len, err, cnt_sel, logits, lse_buf, keys, plan_idx, plan_phys, plan_count, plan_stamp, stage_q, stage_k,
+        stage_v, stage_out, total;
+    int max_units, plan_cap, n_delta, max_pages;
 };
 
 int num_sms_current() {
@@ -39,8 +40,11 @@ int num_sms_current() {
     return sms > 0 ? sms : 148;
 }
 
+// Split-K CTAs per (sequence, kv head) = cluster size: about two CTAs per SM in total (the
+// shallow-ring kernel fits two per SM), at most 16 (one cluster).
 int nsplit_full(int batch, int g, int sms, int max_pages) {
-    int n = (2 * sms) / std::max(1, batch * g);
+    const int heads = std::max(1, batch * g);
+    int n = (2 * sms + heads - 1) / heads;
     n = std::max(1, std::min(n, kMaxSplit));
     return std::min(n, std::max(1, max_pages));
 }
@@ -54,6 +58,9 @@ int nsplit_sparse(const delta_config& c, int batch, int sms, int max_pages, int 
     const int by_tiles = std::max(1, (plan_tiles(c, plan_cap) + 3) / 4);  // >= one 4-tile stage each
     return std::max(1, std::min(full, by_tiles));
 }
+
+// The deep-ring variant (one CTA per SM) is kept for experiments (DELTA_TUNE deep=1).
+bool deep_ring(int, int, int, int) { return false; }
 
 int elem_bytes(const delta_config& c) { return c.kv_dtype == DELTA_BF16 ? 2 : 4; }
 
@@ -119,26 +126,18 @@ Layout layout(const delta_config& c, int sms) {
         const int win_units = c.n_window > 0 ? (blk == 1 ? c.n_window : (c.n_window - 1) / blk + 2) : 0;
         L.plan_cap = std::max(1, std::min(L.max_units, k_units + sink_units + win_units));
     }
-    int rows = 0;
-    for (int b = 1; b <= c.max_batch; ++b)
-        rows = std::max(rows, b * std::max(nsplit_full(b, g, sms, L.max_pages),
-                                           nsplit_sparse(c, b, sms, L.max_pages, L.plan_cap)));
-    L.rows_max = rows;
     const bool has_sel = c.num_select_layers > 0;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + std::max<size_t>(bytes, 1)); return o; };
     L.seq_len = take((size_t)c.num_layers * c.max_batch * 4);
     L.err = take(16);
-    L.cnt_head = take((size_t)c.num_layers * c.max_batch * g * 4);
-    L.cnt_seq = take((size_t)c.num_layers * c.max_batch * 4);
     L.cnt_sel = take((size_t)c.num_layers * c.max_batch * 4);
-    L.part_o = take((size_t)rows * m * D * 4);
-    L.part_lse = take((size_t)rows * m * 4);
     L.logits = take(has_sel ? (size_t)c.max_batch * c.max_seq_len * m * 4 : 0);
     L.lse_buf = take((size_t)c.max_batch * m * 4);
     L.keys = take(has_sel ? (size_t)c.max_batch * L.max_units * 4 : 0);
     const int nd = std::max(1, L.n_delta);
     L.plan_idx = take((size_t)nd * c.max_batch * L.plan_cap * 4);
+    L.plan_phys = take((size_t)nd * c.max_batch * L.plan_cap * 4);
     L.plan_count = take((size_t)nd * c.max_batch * 4);
     L.plan_stamp = take((size_t)nd * c.max_batch * 4);
     L.stage_q = take((size_t)c.num_layers * c.max_batch * m * D * e);
@@ -155,6 +154,28 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
 
 }  // namespace
 
+namespace delta {
+int cluster_limit(const void* kern, int threads, int smem_bytes) {
+    for (int cs = kMaxSplit; cs > 1; cs /= 2) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cs, 1, 1);
+        cfg.blockDim = dim3(threads, 1, 1);
+        cfg.dynamicSmemBytes = smem_bytes;
+        cudaLaunchAttribute a;
+        a.id = cudaLaunchAttributeClusterDimension;
+        a.val.clusterDim.x = cs;
+        a.val.clusterDim.y = 1;
+        a.val.clusterDim.z = 1;
+        cfg.attrs = &a;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) return cs;
+        cudaGetLastError();
+    }
+    return 1;
+}
+}  // namespace delta
+
 struct delta_ctx {
     delta_config cfg;
     std::vector<int32_t> select_layers;
@@ -162,10 +183,9 @@ struct delta_ctx {
     Layout L;
     int sms = 148, gs = 1;
     uint8_t* ws = nullptr;
-    void* k_pool = nullptr;
-    void* v_pool = nullptr;
+    void* kv_pool = nullptr;
     const int32_t* block_table = nullptr;
-    CUtensorMap tm_k, tm_v;
+    CUtensorMap tm_kv;
     bool use_tc = false;
     float scale = 0.f;
     std::vector<long long> step, dec_step, sel_step;
@@ -176,6 +196,11 @@ struct delta_ctx {
     uint64_t graph_kernels = 0;
     uint64_t launches = 0;
     bool pdl = true;
+    int tune_nsplit = 0, tune_deep = -1;  // DELTA_TUNE overrides (0 / -1 = automatic)
+    // the previous kernel this handle enqueued (decides whether the next attention kernel
+    // may start its KV stream before griddepcontrol.wait; see attn_tc.cu)
+    enum { kLastNone, kLastAttn, kLastSelect, kLastAppend } last_kind = kLastNone;
+    int last_layer = -1;
     std::string msg;
 
     template <typename T>
@@ -202,22 +227,23 @@ AttnParams attn_params(delta_ctx* h, int layer, int batch) {
     p.max_batch = c.max_batch; p.max_seq = c.max_seq_len;
     p.sel_block = c.select_block; p.plan_cap = h->L.plan_cap;
     p.scale = h->scale; p.scale_log2 = (float)((double)h->scale * 1.4426950408889634);
-    p.k_pool = h->k_pool; p.v_pool = h->v_pool; p.block_table = h->block_table;
+    p.kv_pool = h->kv_pool; p.block_table = h->block_table;
     p.seq_len = h->at<int32_t>(h->L.seq_len);
-    p.part_o = h->at<float>(h->L.part_o); p.part_lse = h->at<float>(h->L.part_lse);
-    p.cnt_head = h->at<int32_t>(h->L.cnt_head) + (size_t)layer * c.max_batch * c.num_kv_heads;
-    p.cnt_seq = h->at<int32_t>(h->L.cnt_seq) + (size_t)layer * c.max_batch;
     p.logits = h->at<float>(h->L.logits); p.lse_buf = h->at<float>(h->L.lse_buf);
     p.err = h->at<int32_t>(h->L.err);
     if (p.role == kRoleSparse) {
         const int sl = h->slot[h->gov[layer]];
         p.plan_idx = h->at<int32_t>(h->L.plan_idx) + (size_t)sl * c.max_batch * h->L.plan_cap;
+        p.plan_phys = h->at<int32_t>(h->L.plan_phys) + (size_t)sl * c.max_batch * h->L.plan_cap;
         p.plan_count = h->at<int32_t>(h->L.plan_count) + (size_t)sl * c.max_batch;
         p.plan_stamp = h->at<int32_t>(h->L.plan_stamp) + (size_t)sl * c.max_batch;
         p.nsplit = nsplit_sparse(c, batch, h->sms, h->L.max_pages, h->L.plan_cap);
     } else {
         p.nsplit = nsplit_full(batch, c.num_kv_heads, h->sms, h->L.max_pages);
     }
+    if (h->tune_nsplit > 0) p.nsplit = std::min(h->tune_nsplit, kMaxSplit);
+    p.deep = deep_ring(batch, c.num_kv_heads, p.nsplit, h->sms) ? 1 : 0;
+    if (h->tune_deep >= 0) p.deep = h->tune_deep;
     return p;
 }
 
@@ -247,10 +273,20 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
     p.q = q; p.out = out; p.lse_out = lse_out;
     p.fuse_append = (k_new != nullptr);
     p.k_new = k_new; p.v_new = v_new;
-    cudaError_t e = h->use_tc ? launch_attn_tc(p, &h->tm_k, &h->tm_v, st, h->pdl)
+    // May the kernel read its length counter, block table and plan before the previous kernel
+    // completes?  Not if that kernel is this layer's own (append / attention: the counter) or
+    // the select that wrote this sparse layer's plan.
+    p.prewait = 1;
+    if (h->last_layer == layer && (h->last_kind == delta_ctx::kLastAppend || h->last_kind == delta_ctx::kLastAttn))
+        p.prewait = 0;
+    if (p.role == kRoleSparse && h->last_kind == delta_ctx::kLastSelect && h->last_layer == h->gov[layer])
+        p.prewait = 0;
+    cudaError_t e = h->use_tc ? launch_attn_tc(p, &h->tm_kv, st, h->pdl)
                               : launch_attn_simt(p, h->cfg.kv_dtype == DELTA_BF16, st, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "decode launch");
     ++h->launches;
+    h->last_kind = delta_ctx::kLastAttn;
+    h->last_layer = layer;
     return DELTA_OK;
 }
 
@@ -259,7 +295,7 @@ delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_ov
     const delta_config& c = h->cfg;
     SelectParams p = {};
     const int sl = h->slot[layer];
-    p.m = c.num_q_heads; p.layer = layer; p.batch = batch;
+    p.m = c.num_q_heads; p.g = c.num_kv_heads; p.layer = layer; p.batch = batch;
     p.nchunk = std::max(1, std::min((h->L.max_units + 15) / 16, (2 * h->sms + batch - 1) / batch));
     p.sel_block = c.select_block; p.n_sink = c.n_sink; p.n_window = c.n_window;
     p.k_units = c.budget_k / c.select_block;
@@ -268,6 +304,8 @@ delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_ov
     p.logits = h->at<float>(h->L.logits); p.lse_buf = h->at<float>(h->L.lse_buf);
     p.keys_override = keys_override; p.keys = h->at<float>(h->L.keys);
     p.plan_idx = h->at<int32_t>(h->L.plan_idx) + (size_t)sl * c.max_batch * h->L.plan_cap;
+    p.plan_phys = h->at<int32_t>(h->L.plan_phys) + (size_t)sl * c.max_batch * h->L.plan_cap;
+    p.block_table = h->block_table; p.bt_stride = h->L.max_pages;
     p.plan_count = h->at<int32_t>(h->L.plan_count) + (size_t)sl * c.max_batch;
     p.plan_stamp = h->at<int32_t>(h->L.plan_stamp) + (size_t)sl * c.max_batch;
     p.idx_out = idx_out; p.count_out = count_out;
@@ -276,6 +314,8 @@ delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_ov
     cudaError_t e = launch_select(p, st, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "select launch");
     ++h->launches;
+    h->last_kind = delta_ctx::kLastSelect;
+    h->last_layer = layer;
     return DELTA_OK;
 }
 
@@ -315,7 +355,7 @@ extern "C" {
 
 const char* delta_version(void) { return "delta-b200 0.1 (sm_100a)"; }
 
-delta_status delta_query_sizes(const delta_config* cfg, size_t* pool_bytes_each, size_t* workspace_bytes) {
+delta_status delta_query_sizes(const delta_config* cfg, size_t* kv_pool_bytes, size_t* workspace_bytes) {
     if (!cfg) return fail(nullptr, DELTA_ERR_CONFIG, "null config");
     std::vector<int> role, gov;
     std::string err = validate(*cfg, role, gov);
@@ -323,8 +363,8 @@ delta_status delta_query_sizes(const delta_config* cfg, size_t* pool_bytes_each,
     delta_config c = *cfg;
     const int max_pages = (c.max_seq_len + kPage - 1) / kPage;
     const long long phys = c.num_phys_pages > 0 ? c.num_phys_pages : (long long)c.max_batch * max_pages;
-    if (pool_bytes_each)
-        *pool_bytes_each = (size_t)c.num_layers * phys * c.num_kv_heads * kPage * c.head_dim * elem_bytes(c);
+    if (kv_pool_bytes)
+        *kv_pool_bytes = (size_t)c.num_layers * phys * c.num_kv_heads * 2 * kPage * c.head_dim * elem_bytes(c);
     if (workspace_bytes) *workspace_bytes = layout(c, num_sms_current()).total;
     return DELTA_OK;
 }
@@ -348,7 +388,7 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
     h->gs = cfg->num_q_heads / cfg->num_kv_heads;
     h->L = layout(h->cfg, h->sms);
     h->scale = cfg->softmax_scale > 0.f ? cfg->softmax_scale : (float)(1.0 / std::sqrt((double)cfg->head_dim));
-    if (!bufs->k_pool || !bufs->v_pool || !bufs->block_table || !bufs->workspace) {
+    if (!bufs->kv_pool || !bufs->block_table || !bufs->workspace) {
         delete h;
         return fail(nullptr, DELTA_ERR_USAGE, "null buffer");
     }
@@ -356,17 +396,16 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
         delete h;
         return fail(nullptr, DELTA_ERR_CAPACITY, "workspace too small: need " + std::to_string(h->L.total));
     }
-    if (reinterpret_cast<uintptr_t>(bufs->workspace) % kAlign || reinterpret_cast<uintptr_t>(bufs->k_pool) % 1024 ||
-        reinterpret_cast<uintptr_t>(bufs->v_pool) % 1024) {
+    if (reinterpret_cast<uintptr_t>(bufs->workspace) % kAlign || reinterpret_cast<uintptr_t>(bufs->kv_pool) % 1024) {
         delete h;
-        return fail(nullptr, DELTA_ERR_USAGE, "workspace must be 256-byte and pools 1024-byte aligned");
+        return fail(nullptr, DELTA_ERR_USAGE, "workspace must be 256-byte and kv_pool 1024-byte aligned");
     }
     h->ws = static_cast<uint8_t*>(bufs->workspace);
-    h->k_pool = bufs->k_pool; h->v_pool = bufs->v_pool; h->block_table = bufs->block_table;
+    h->kv_pool = bufs->kv_pool; h->block_table = bufs->block_table;
     h->use_tc = (cfg->kv_dtype == DELTA_BF16);
     if (h->use_tc) {
-        const unsigned long long rows =
-            (unsigned long long)cfg->num_layers * h->cfg.num_phys_pages * cfg->num_kv_heads * kPage;
+        const unsigned long long rows =  // rows of d elements in the pool (K and V rows)
+            (unsigned long long)cfg->num_layers * h->cfg.num_phys_pages * cfg->num_kv_heads * 2 * kPage;
         if (rows >= (1ull << 31)) {
             delete h;
             return fail(nullptr, DELTA_ERR_CONFIG, "pool too large for 32-bit TMA row coordinates");
@@ -379,19 +418,22 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
             return fail(nullptr, DELTA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
         }
         auto encode = reinterpret_cast<PFN_encodeTiled>(fn);
-        const cuuint64_t dims[2] = {(cuuint64_t)cfg->head_dim, (cuuint64_t)rows};
-        const cuuint64_t strides[1] = {(cuuint64_t)cfg->head_dim * 2};
-        const cuuint32_t box[2] = {64, (cuuint32_t)kPage};
-        const cuuint32_t estr[2] = {1, 1};
-        for (int i = 0; i < 2; ++i) {
-            CUresult r = encode(i == 0 ? &h->tm_k : &h->tm_v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                                i == 0 ? bufs->k_pool : bufs->v_pool, dims, strides, box, estr,
-                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (r != CUDA_SUCCESS) {
-                delete h;
-                return fail(nullptr, DELTA_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-            }
+        // One box = one (page, head): its P K rows and P V rows (2P rows x d), i.e. one 4 KiB
+        // (d = 64) or 8 KiB (d = 128) request.  d = 64: 2-D {64, rows}.  d = 128: 3-D
+        // {64, 2, rows} so a single request covers both 128-byte halves of each row under the
+        // 128B swizzle (the inner box extent is limited to 128 bytes).
+        const bool d128 = cfg->head_dim == 128;
+        const cuuint32_t rank = d128 ? 3 : 2;
+        const cuuint64_t dims[3] = {64, d128 ? 2ull : (cuuint64_t)rows, (cuuint64_t)rows};
+        const cuuint64_t strides[2] = {128ull, 256ull};
+        const cuuint32_t box[3] = {64, d128 ? 2u : (cuuint32_t)(2 * kPage), (cuuint32_t)(2 * kPage)};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = encode(&h->tm_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, bufs->kv_pool, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            delete h;
+            return fail(nullptr, DELTA_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
         }
     }
     cudaError_t e = cudaMemset(h->ws, 0, h->L.total);
@@ -400,6 +442,13 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
         std::string m = std::string("workspace init: ") + cudaGetErrorString(e);
         delete h;
         return fail(nullptr, DELTA_ERR_CUDA, m);
+    }
+    // Tuning hook for kernel experiments (tools/trace_probe.py): DELTA_TUNE="nsplit=N,deep=0|1".
+    if (const char* t = std::getenv("DELTA_TUNE")) {
+        const char* a = std::strstr(t, "nsplit=");
+        const char* d = std::strstr(t, "deep=");
+        if (a) h->tune_nsplit = std::atoi(a + 7);
+        if (d) h->tune_deep = std::atoi(d + 5);
     }
     h->step.assign(cfg->num_layers, 0);
     h->dec_step.assign(cfg->num_layers, -1);
@@ -424,9 +473,11 @@ delta_status delta_set_seq_lens(delta_t h, int32_t layer, int32_t batch, const i
         if (lens_host[b] < 0 || lens_host[b] > h->cfg.max_seq_len)
             return fail(h, DELTA_ERR_CAPACITY, "length exceeds max_seq_len");
     int32_t* sl = h->at<int32_t>(h->L.seq_len);
+    std::vector<int32_t> raw(lens_host, lens_host + batch);  // device counters hold n * g (combine.cuh)
+    for (auto& x : raw) x *= h->cfg.num_kv_heads;
     const int l0 = layer < 0 ? 0 : layer, l1 = layer < 0 ? h->cfg.num_layers : layer + 1;
     for (int l = l0; l < l1; ++l) {
-        cudaError_t e = cudaMemcpyAsync(sl + (size_t)l * h->cfg.max_batch, lens_host, sizeof(int32_t) * batch,
+        cudaError_t e = cudaMemcpyAsync(sl + (size_t)l * h->cfg.max_batch, raw.data(), sizeof(int32_t) * batch,
                                         cudaMemcpyHostToDevice, stream);
         if (e != cudaSuccess) return cuda_fail(h, e, "set_seq_lens");
     }
@@ -447,11 +498,13 @@ delta_status delta_append_kv(delta_t h, int32_t layer, int32_t batch, int32_t nt
     p.g = h->cfg.num_kv_heads; p.d = h->cfg.head_dim; p.layer = layer; p.batch = batch; p.ntok = ntok;
     p.num_phys = h->cfg.num_phys_pages; p.bt_stride = h->L.max_pages; p.max_batch = h->cfg.max_batch;
     p.max_seq = h->cfg.max_seq_len; p.elem_bytes = elem_bytes(h->cfg);
-    p.k_new = k_new; p.v_new = v_new; p.k_pool = h->k_pool; p.v_pool = h->v_pool;
+    p.k_new = k_new; p.v_new = v_new; p.kv_pool = h->kv_pool;
     p.block_table = h->block_table; p.seq_len = h->at<int32_t>(h->L.seq_len); p.err = h->at<int32_t>(h->L.err);
     cudaError_t e = launch_append(p, stream, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "append launch");
     ++h->launches;
+    h->last_kind = delta_ctx::kLastAppend;
+    h->last_layer = layer;
     h->step[layer] += 1;
     return DELTA_OK;
 }

@@ -12,7 +12,15 @@ enum DevErr : int { kDevOk = 0, kDevUsage = 2, kDevNumeric = 3, kDevCapacity = 4
 
 constexpr int kPage = 16;        // P
 constexpr int kMaxGs = 16;       // query heads per KV group handled by one MMA row tile
-constexpr int kMaxSplit = 64;    // split-K partials per (sequence, kv head)
+constexpr int kMaxSplit = 16;    // split-K CTAs per (sequence, kv head) = one thread-block cluster
+
+// Row (of d elements) holding slot `slot` of the K head-page of (layer_page, head h), where
+// layer_page = layer * num_phys + physical page; the matching V row is kv_row(...) + kPage.
+// Pool layout [L][num_phys][g][2][P][d]: one (page, head) is 2P contiguous rows (K then V),
+// so a single 4-8 KiB TMA request fetches both (per-SM TMA throughput is request-bound).
+__host__ __device__ __forceinline__ size_t kv_row(size_t layer_page, int g, int h, int slot) {
+    return ((layer_page * (size_t)g + (size_t)h) * 2) * kPage + (size_t)slot;
+}
 
 // One decode-attention launch (one layer, sequences [0, batch)).
 struct AttnParams {
@@ -24,24 +32,22 @@ struct AttnParams {
     int sel_block;      // SPARSE: 1 = token plan, P = page plan
     int plan_cap;       // plan row stride (units)
     int fuse_append;    // 1: append k_new/v_new at position seq_len (pre) in this launch
+    int deep;           // 1: one CTA per SM with the deep TMA ring (few CTAs), 0: shallow ring
+    int prewait;        // 1: start geometry + KV stream before griddepcontrol.wait (see attn_tc.cu)
     float scale;        // softmax scale (natural units)
     float scale_log2;   // scale * log2(e)
     const void* q;      // [batch][m][d]
     const void* k_new;  // [batch][g][d] (fuse_append)
     const void* v_new;
-    void* k_pool;       // [L][num_phys][g][P][d]
-    void* v_pool;
+    void* kv_pool;      // [L][num_phys][g][2][P][d]: K rows then V rows of each (page, head)
     const int32_t* block_table;   // [max_batch][bt_stride]
-    int32_t* seq_len;   // [L][max_batch]
+    int32_t* seq_len;   // [L][max_batch] raw length counters: n * g (see combine.cuh)
     float* out;         // [batch][m][d]
     float* lse_out;     // [batch][m] or null
-    float* part_o;      // [batch][g][nsplit][gs][d]
-    float* part_lse;    // [batch][g][nsplit][gs]  (log2 units)
-    int32_t* cnt_head;  // [max_batch][g] (this layer)
-    int32_t* cnt_seq;   // [max_batch]    (this layer)
     float* logits;      // SELECT: [max_batch][max_seq][m] (natural units, scaled)
     float* lse_buf;     // SELECT: [max_batch][m] natural-log LSE for the score pass
-    const int32_t* plan_idx;    // SPARSE: [max_batch][plan_cap]
+    const int32_t* plan_idx;    // SPARSE: [max_batch][plan_cap] unit ids (pages or tokens)
+    const int32_t* plan_phys;   // SPARSE: same shape: physical page (page plan) or page*P+slot (token plan)
     const int32_t* plan_count;  // [max_batch]
     const int32_t* plan_stamp;  // [max_batch]
     int32_t* err;
@@ -49,15 +55,18 @@ struct AttnParams {
 
 // Score + top-k selection launch (one Delta layer).
 struct SelectParams {
-    int m, layer, batch, nchunk;
+    int m, g, layer, batch, nchunk;
     int sel_block, n_sink, n_window, k_units;
     int max_batch, max_seq, max_units, plan_cap;
-    const int32_t* seq_len;     // [L][max_batch]
+    const int32_t* seq_len;     // [L][max_batch] raw counters n * g
     const float* logits;        // [max_batch][max_seq][m]
     const float* lse_buf;       // [max_batch][m]
     const float* keys_override; // [batch][ceil(s/sel_block)] or null
     float* keys;                // [max_batch][max_units] scratch
     int32_t* plan_idx;          // [max_batch][plan_cap]
+    int32_t* plan_phys;         // [max_batch][plan_cap] physical page / page*P+slot of each unit
+    const int32_t* block_table; // [max_batch][bt_stride]
+    int bt_stride;
     int32_t* plan_count;
     int32_t* plan_stamp;
     int32_t* idx_out;           // optional [batch][plan_cap]
@@ -70,8 +79,7 @@ struct AppendParams {
     int g, d, layer, batch, ntok, num_phys, bt_stride, max_batch, max_seq, elem_bytes;
     const void* k_new;  // [batch][ntok][g][d]
     const void* v_new;
-    void* k_pool;
-    void* v_pool;
+    void* kv_pool;
     const int32_t* block_table;
     int32_t* seq_len;
     int32_t* err;
@@ -79,11 +87,12 @@ struct AppendParams {
 
 // Launchers (attn_tc.cu / attn_simt.cu / select.cu / append.cu).  Each returns the
 // cudaError_t of the launch.  `pdl` enables programmatic dependent launch.
-cudaError_t launch_attn_tc(const AttnParams& p, const CUtensorMap* tm_k, const CUtensorMap* tm_v,
-                           cudaStream_t st, bool pdl);
+cudaError_t launch_attn_tc(const AttnParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl);
 cudaError_t launch_attn_simt(const AttnParams& p, bool bf16, cudaStream_t st, bool pdl);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t st, bool pdl);
 cudaError_t launch_append(const AppendParams& p, cudaStream_t st, bool pdl);
 size_t select_smem_bytes(int max_units);
+// Largest cluster size (16, 8, 4, 2 or 1) with which `kern` can be resident (delta_api.cu).
+int cluster_limit(const void* kern, int threads, int smem_bytes);
 
 }  // namespace delta

@@ -6,6 +6,21 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#ifdef DELTA_TRACE
+// Phase timestamps (%globaltimer, ns) per CTA for latency analysis; trace builds only
+// (`make trace`), never the product library.
+static __device__ unsigned long long g_delta_trace[8192 * 12];
+#define DTRACE(slot)                                                                          \
+    do {                                                                                      \
+        unsigned long long t_;                                                                \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                \
+        const unsigned cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+        if (cta_ < 8192) g_delta_trace[cta_ * 12 + (slot)] = t_;                               \
+    } while (0)
+#else
+#define DTRACE(slot) do {} while (0)
+#endif
+
 namespace delta {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -29,13 +44,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+// No suspend-time hint: with a hint the waiting warp is parked and woken late (measured
+// ~0.6 us per stage on B200), which throttles a TMA ring far below its in-flight capacity.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(0x989680u)
+        "r"(parity)
         : "memory");
 }
 // cp.async completion tracked by an mbarrier (one pending arrival per calling thread).
@@ -57,6 +74,15 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
         "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m, uint64_t* bar,
+                                            int c0, int c1, int c2, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
         : "memory");
 }
 
@@ -87,12 +113,21 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
                  : "r"(addr));
 }
 // D += A(16x16, row) * B(16x8, col), bf16 inputs, fp32 accumulate.
+// Not volatile: a pure function of its register operands, so the compiler may interleave
+// independent MMAs (ldmatrix stays volatile: it must not move above the stage barrier).
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Transpose of an 8x8 b16 matrix held one bf16x2 per lane (lane g*4+t: row g, cols 2t, 2t+1).
+__device__ __forceinline__ uint32_t movmatrix_trans(uint32_t a) {
+    uint32_t d;
+    asm("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+    return d;
 }
 
 // ------------------------------------------------------------------ PDL

@@ -56,6 +56,41 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scratch, int* total) 
     return warp_excl + x - v;
 }
 
+// max_j (a_j(t) - LSE_j) over the heads j this lane owns: lane pair (hh = 0, 1) splits the m
+// heads of token t.  m % 4 == 0: 16-byte loads, all issued before the max chain (the row is
+// 16-byte aligned because the logits are [s][m] fp32).  Max is exact, so the split and the
+// order do not change the result.
+__device__ __forceinline__ float head_max(const float* __restrict__ row, const float* lse_s, int m, int hh) {
+    float mx = -INFINITY;
+    if ((m & 3) == 0) {
+        const float4* r4 = reinterpret_cast<const float4*>(row);
+        const int n4 = m >> 2;
+        float4 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int q = hh + 2 * i;
+            v[i] = q < n4 ? r4[q] : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int q = hh + 2 * i;
+            if (q < n4) {
+                mx = fmaxf(mx, fmaxf(fmaxf(v[i].x - lse_s[4 * q], v[i].y - lse_s[4 * q + 1]),
+                                     fmaxf(v[i].z - lse_s[4 * q + 2], v[i].w - lse_s[4 * q + 3])));
+            }
+        }
+        for (int q = hh + 16; q < n4; q += 2) {
+            const float4 w = r4[q];
+            mx = fmaxf(mx, fmaxf(fmaxf(w.x - lse_s[4 * q], w.y - lse_s[4 * q + 1]),
+                                 fmaxf(w.z - lse_s[4 * q + 2], w.w - lse_s[4 * q + 3])));
+        }
+    } else {
+#pragma unroll 8
+        for (int j = hh; j < m; j += 2) mx = fmaxf(mx, row[j] - lse_s[j]);
+    }
+    return mx;
+}
+
 __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams p) {
     extern __shared__ uint32_t sm_keys[];  // [kSmemUnits] (only when it fits)
     __shared__ float lse_s[256];
@@ -67,7 +102,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
     const int b = blockIdx.y;
     pdl_wait();
 
-    const int s = p.seq_len[p.layer * p.max_batch + b];
+    const int s = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
     const int block = p.sel_block;
     const int n_units = (s + block - 1) / block;
     float* keys_b = p.keys + (size_t)b * p.max_units;
@@ -80,16 +115,13 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
         const int per = (n_units + p.nchunk - 1) / p.nchunk;
         const int u_lo = blockIdx.x * per, u_hi = min(n_units, u_lo + per);
         const float* lg = p.logits + (size_t)b * p.max_seq * p.m;
-        const int half_m = (p.m + 1) >> 1;
         const int jr = lane >> 1, hh = lane & 1;
-        const int j0 = hh * half_m, j1 = min(p.m, j0 + half_m);
         // a warp handles 16 consecutive tokens: lane = 2*token + half-of-heads
         if (block == kPage) {
             for (int u = u_lo + warp; u < u_hi; u += kSelWarps) {
                 const int t = u * kPage + jr;
                 float mx = -INFINITY;
-                if (t < s)
-                    for (int j = j0; j < j1; ++j) mx = fmaxf(mx, lg[(size_t)t * p.m + j] - lse_s[j]);
+                if (t < s) mx = head_max(lg + (size_t)t * p.m, lse_s, p.m, hh);
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
                 const float e = (t < s) ? expf(mx) : 0.f;
                 float sum = 0.f;
@@ -102,8 +134,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
             for (int t0 = t_lo + warp * 16; t0 < t_hi; t0 += kSelWarps * 16) {
                 const int t = t0 + jr;
                 float mx = -INFINITY;
-                if (t < t_hi)
-                    for (int j = j0; j < j1; ++j) mx = fmaxf(mx, lg[(size_t)t * p.m + j] - lse_s[j]);
+                if (t < t_hi) mx = head_max(lg + (size_t)t * p.m, lse_s, p.m, hh);
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
                 if (t < t_hi && hh == 0) keys_b[t] = mx;
             }
@@ -120,6 +151,10 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
 
     // ------------------------------------------------------------ phase B: top-k
     int32_t* plan = p.plan_idx + (size_t)b * p.plan_cap;
+    int32_t* plan_phys = p.plan_phys + (size_t)b * p.plan_cap;
+    const int32_t* bt = p.block_table + (size_t)b * p.bt_stride;
+    // physical location of a unit for the sparse kernels: page id, or page * P + slot (tokens)
+    auto phys_of = [&](int u) -> int32_t { return block == 1 ? bt[u / kPage] * kPage + (u % kPage) : bt[u]; };
     const int S = p.n_sink, L = p.n_window;
     const int sink_hi = (S > 0 && s > 0) ? (min(S, s) - 1) / block + 1 : 0;
     const int win_lo = (L > 0) ? max(0, s - L) / block : n_units;
@@ -129,7 +164,10 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
     int count = 0;
 
     if (n_cand <= p.k_units) {
-        for (int u = tid; u < n_units; u += kSelThreads) plan[u] = u;  // R12: budget covers all
+        for (int u = tid; u < n_units; u += kSelThreads) {  // R12: budget covers all
+            plan[u] = u;
+            plan_phys[u] = phys_of(u);
+        }
         count = n_units;
     } else {
         const bool cached = n_units <= kSmemUnits;
@@ -160,38 +198,80 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
                     if ((v & maskbits) == prefix) atomicAdd(&hist[(v >> shift) & 255], 1);
                 }
                 __syncthreads();
-                const int c = (tid < 256) ? hist[255 - tid] : 0;  // bins in descending order
-                int tot;
-                const int excl = block_excl_scan(c, scratch, &tot);
-                if (tid < 256 && excl < remaining && excl + c >= remaining) {
-                    s_bin = 255 - tid;
-                    s_rem = remaining - excl;
+                if (warp == 0) {  // one warp walks the 256 bins in descending order
+                    int c[8], sum = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        c[k] = hist[255 - (lane * 8 + k)];
+                        sum += c[k];
+                    }
+                    int incl = sum;
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, off);
+                        if (lane >= off) incl += y;
+                    }
+                    int excl = incl - sum;
+                    if (excl < remaining && incl >= remaining) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            if (excl + c[k] >= remaining) {
+                                s_bin = 255 - (lane * 8 + k);
+                                s_rem = remaining - excl;
+                                break;
+                            }
+                            excl += c[k];
+                        }
+                    }
                 }
                 __syncthreads();
                 prefix |= (uint32_t)s_bin << shift;
                 maskbits |= 0xFFu << shift;
                 remaining = s_rem;
-                __syncthreads();
             }
         }
         const uint32_t T = prefix;
         const int need_eq = remaining;  // keys equal to T still to take (lowest index first)
         const bool take_any = p.k_units > 0;
+        constexpr int IPT = 8;          // consecutive units per thread: one chunk = 4096 units
         int carry_eq = 0, carry_pos = 0;
-        for (int base = 0; base < n_units; base += kSelThreads) {
-            const int u = base + tid;
-            const bool valid = u < n_units;
-            const bool f = valid && forced(u);
-            uint32_t v = 0;
-            if (valid && !f) v = K(u);
-            const bool cand = valid && !f && take_any;
-            const bool is_gt = cand && v > T;
-            const bool is_eq = cand && v == T;
+        for (int base = 0; base < n_units; base += kSelThreads * IPT) {
+            const int u0 = base + tid * IPT;
+            uint32_t fl_f = 0, fl_gt = 0, fl_eq = 0;  // bit i: unit u0 + i is forced / > T / == T
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                const int u = u0 + i;
+                if (u < n_units) {
+                    if (forced(u)) {
+                        fl_f |= 1u << i;
+                    } else if (take_any) {
+                        const uint32_t v = K(u);
+                        if (v > T) fl_gt |= 1u << i;
+                        else if (v == T) fl_eq |= 1u << i;
+                    }
+                }
+            }
             int tot_eq, tot_sel;
-            const int eq_rank = block_excl_scan(is_eq ? 1 : 0, scratch, &tot_eq) + carry_eq;
-            const bool sel = f || is_gt || (is_eq && eq_rank < need_eq);
-            const int pos = block_excl_scan(sel ? 1 : 0, scratch, &tot_sel) + carry_pos;
-            if (sel && pos < p.plan_cap) plan[pos] = u;
+            int eq_rank = block_excl_scan(__popc(fl_eq), scratch, &tot_eq) + carry_eq;
+            uint32_t fl_sel = fl_f | fl_gt;
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                if (fl_eq & (1u << i)) {
+                    if (eq_rank < need_eq) fl_sel |= 1u << i;
+                    ++eq_rank;
+                }
+            }
+            int pos = block_excl_scan(__popc(fl_sel), scratch, &tot_sel) + carry_pos;
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                if (fl_sel & (1u << i)) {
+                    if (pos < p.plan_cap) {
+                        plan[pos] = u0 + i;
+                        plan_phys[pos] = phys_of(u0 + i);
+                    }
+                    ++pos;
+                }
+            }
             carry_eq += tot_eq;
             carry_pos += tot_sel;
         }

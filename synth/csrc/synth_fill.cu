@@ -43,12 +43,13 @@ __device__ __forceinline__ float round_bf16(float x) {
     return __uint_as_float(u);
 }
 
-// pool [L][num_phys][g][P][d]; fills logical rows t < s_fill of layers [layer0, layer0+nl),
-// sequences [0, batch).  plant_mask: [nl][batch][plant_stride] (unit = t / plant_block).
+// pool [L][num_phys][g][kv_slots][P][d]; fills logical rows t < s_fill of layers
+// [layer0, layer0+nl), sequences [0, batch), into slot `kv_slot` (0 = K, 1 = V when the pool
+// interleaves K and V per (page, head)).  plant_mask: [nl][batch][plant_stride].
 __global__ void fill_pool_kernel(void* pool, int bf16, uint64_t seed, int tag, int layer0, int batch, int s_fill,
                                  int g, int d, int P, int num_phys, const int32_t* bt, int bt_stride,
                                  const uint8_t* plant_mask, int plant_block, int plant_stride, const float* sigma,
-                                 float B) {
+                                 float B, int kv_slots, int kv_slot) {
     const int ls = blockIdx.y;  // (layer offset, seq)
     const int li = ls / batch, b = ls % batch;
     const int layer = layer0 + li;
@@ -65,7 +66,8 @@ __global__ void fill_pool_kernel(void* pool, int bf16, uint64_t seed, int tag, i
             x = __fadd_rn(x, __fmul_rn(B, sigma[((size_t)li * batch + b) * d + e]));
             if (bf16) x = round_bf16(x);
         }
-        const size_t row = (((size_t)layer * num_phys + bt[(size_t)b * bt_stride + t / P]) * g + h) * P + (t % P);
+        const size_t row =
+            ((((size_t)layer * num_phys + bt[(size_t)b * bt_stride + t / P]) * g + h) * kv_slots + kv_slot) * P + (t % P);
         if (bf16)
             reinterpret_cast<__nv_bfloat16*>(pool)[row * d + e] = __float2bfloat16_rn(x);  // exact
         else
@@ -110,7 +112,8 @@ extern "C" {
 
 int synth_fill_pool(void* pool, int bf16, uint64_t seed, int tag, int layer0, int nl, int batch, int s_fill, int g,
                     int d, int P, int num_phys, const int32_t* bt, int bt_stride, const uint8_t* plant_mask,
-                    int plant_block, int plant_stride, const float* sigma, float B, cudaStream_t st) {
+                    int plant_block, int plant_stride, const float* sigma, float B, int kv_slots, int kv_slot,
+                    cudaStream_t st) {
     if (s_fill <= 0) return 0;
     const long long n = (long long)s_fill * g * d;
     const int threads = 256;
@@ -118,7 +121,8 @@ int synth_fill_pool(void* pool, int bf16, uint64_t seed, int tag, int layer0, in
     if (blocks > 4096) blocks = 4096;
     dim3 grid((unsigned)blocks, (unsigned)(nl * batch));
     fill_pool_kernel<<<grid, threads, 0, st>>>(pool, bf16, seed, tag, layer0, batch, s_fill, g, d, P, num_phys, bt,
-                                               bt_stride, plant_mask, plant_block, plant_stride, sigma, B);
+                                               bt_stride, plant_mask, plant_block, plant_stride, sigma, B,
+                                               kv_slots, kv_slot);
     return (int)cudaGetLastError();
 }
 

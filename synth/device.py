@@ -25,7 +25,7 @@ def lib():
         L = ctypes.CDLL(_LIB)
         vp, i32 = ctypes.c_void_p, ctypes.c_int
         L.synth_fill_pool.argtypes = [vp, i32, ctypes.c_uint64, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp, i32,
-                                      vp, i32, i32, vp, ctypes.c_float, vp]
+                                      vp, i32, i32, vp, ctypes.c_float, i32, i32, vp]
         L.synth_fill_rows.argtypes = [vp, i32, ctypes.c_uint64, i32, i32, i32, i32, vp, i32, i32, i32, vp, vp, vp,
                                       ctypes.c_float, vp]
         _lib = L
@@ -49,23 +49,25 @@ def plant_tables(seed, layers, batch, d, planting: Planting | None, n_units: int
     return torch.from_numpy(mask).to(device), torch.from_numpy(sg).to(device)
 
 
-def fill_pools(k_pool, v_pool, block_table, seed: int, s_fill: int, batch: int, layers, planting=None):
-    """Fill logical rows t < s_fill of sequences [0,batch) for the given (contiguous) layers."""
-    L_, phys, g, P, d = k_pool.shape
-    bf16 = 1 if k_pool.dtype == torch.bfloat16 else 0
+def fill_pools(kv_pool, block_table, seed: int, s_fill: int, batch: int, layers, planting=None):
+    """Fill logical rows t < s_fill of sequences [0,batch) for the given (contiguous) layers of a
+    pool [L][phys][g][2][P][d] (K rows then V rows per (page, head))."""
+    L_, phys, g, two, P, d = kv_pool.shape
+    assert two == 2
+    bf16 = 1 if kv_pool.dtype == torch.bfloat16 else 0
     layers = list(layers)
     l0, nl = layers[0], len(layers)
     assert layers == list(range(l0, l0 + nl))
     n_units = -(-s_fill // (planting.block if planting else 1)) if planting else 1
-    mask, sg = plant_tables(seed, layers, batch, d, planting, max(n_units, 1), k_pool.device)
-    for pool, tag in ((k_pool, TAG_K), (v_pool, TAG_V)):
+    mask, sg = plant_tables(seed, layers, batch, d, planting, max(n_units, 1), kv_pool.device)
+    for slot, tag in ((0, TAG_K), (1, TAG_V)):
         use_plant = planting is not None and tag == TAG_K and mask is not None
-        st = lib().synth_fill_pool(pool.data_ptr(), bf16, seed, tag, l0, nl, batch, s_fill, g, d, P, phys,
+        st = lib().synth_fill_pool(kv_pool.data_ptr(), bf16, seed, tag, l0, nl, batch, s_fill, g, d, P, phys,
                                    block_table.data_ptr(), block_table.shape[1],
                                    mask.data_ptr() if use_plant else None,
                                    planting.block if use_plant else 1, mask.shape[2] if use_plant else 1,
                                    sg.data_ptr() if use_plant else None,
-                                   float(planting.B) if use_plant else 0.0, _stream())
+                                   float(planting.B) if use_plant else 0.0, 2, slot, _stream())
         assert st == 0, f"synth_fill_pool failed: {st}"
 
 

@@ -140,7 +140,7 @@ class GpuCase:
         self.cfg = shape.delta_config(batch, max_seq)
         bt = torch.from_numpy(synth.block_table(seed, batch, self.cfg.max_pages))
         self.stack = DeltaStack.allocate(self.cfg, bt)
-        sd.fill_pools(self.stack.k_pool, self.stack.v_pool, self.stack.block_table, seed, s_pre, batch,
+        sd.fill_pools(self.stack.kv_pool, self.stack.block_table, seed, s_pre, batch,
                       range(shape.L), planting)
         self.stack.set_seq_lens([s_pre] * batch)
         self.dt = torch.bfloat16 if shape.dtype == "bf16" else torch.float32

@@ -44,8 +44,8 @@ def _c1(**kw):
 
 def test_query_sizes_c1():
     pool, ws = d200.query_sizes(_c1())
-    # one pool = L x pages x g x P x d x 2 bytes
-    assert pool == 32 * 2052 * 8 * 16 * 128 * 2
+    # kv_pool = L x pages x g x 2 (K, V) x P x d x 2 bytes
+    assert pool == 32 * 2052 * 8 * 2 * 16 * 128 * 2
     assert ws > 0 and ws % 256 == 0
 
 

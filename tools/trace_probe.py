@@ -1,0 +1,114 @@
+"""Latency anatomy of the attention kernel at C1 using the trace build (make trace):
+per-CTA %globaltimer stamps at entry(0), after griddepcontrol.wait(1), first stage landed(2),
+main loop done(3), CTA merge written(4), elected last(5), combine done(6).
+usage: python tools/trace_probe.py   (loads build_trace/libdelta.so)"""
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ["DELTA_LIB_PATH"] = os.environ.get("PROBE_LIB") or os.path.join(ROOT, "build_trace", "libdelta.so")
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2510_09883_b200 as d200  # noqa: E402
+import synth  # noqa: E402
+from synth import device as sd  # noqa: E402
+
+lib = d200.load_library()
+buf = np.zeros(8192 * 12, np.uint64)
+
+
+def read():
+    assert lib.delta_trace_read(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes)) == 0
+    return buf.reshape(8192, 12).astype(np.int64).copy()
+
+
+def report(name, tr):
+    live = tr[:, 0] > 0
+    t = tr[live]
+    t0 = t[:, 0].min()
+    rel = np.where(t > 0, t - t0, -1)
+    n = len(t)
+    last = rel[:, 5] >= 0
+    print(f"== {name}: {n} CTAs, span {(t[t > 0].max() - t0) / 1e3:.2f} us")
+    for k, lab in [(0, "entry"), (1, "pdl_wait done"), (2, "first stage landed"), (3, "loop done"),
+                   (4, "epilogue start"), (5, "cta merge done"), (7, "cluster sync 1"), (8, "peer M/L gathered"),
+                   (9, "outputs written"), (10, "cluster sync 2"), (6, "epilogue done")]:
+        v = rel[:, k][rel[:, k] >= 0] / 1e3
+        if v.size:
+            print(f"   {lab:20s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f} us")
+
+
+def main():
+    ctx = 32768
+    L, m, g, d, F, delta = 32, 32, 8, 128, 2, [2, 16, 25]
+    cfg = d200.DeltaConfig(num_layers=L, num_q_heads=m, num_kv_heads=g, head_dim=d, max_batch=1,
+                           max_seq_len=ctx + 64, num_full_prefix=F, select_layers=delta, budget_k=2048,
+                           n_sink=4, n_window=32, select_block=16)
+    bt = torch.from_numpy(synth.block_table(7, 1, cfg.max_pages))
+    base = d200.DeltaStack.allocate(cfg, bt)
+    sd.fill_pools(base.kv_pool, base.block_table, 7, ctx - 1, 1, range(L))
+    q = torch.empty((L, 1, m, d), dtype=torch.bfloat16, device="cuda")
+    k = torch.empty((L, 1, g, d), dtype=torch.bfloat16, device="cuda")
+    v = torch.empty_like(k)
+    sd.fill_queries(q, 7, range(L), [ctx])
+    sd.fill_new_kv(k, v, 7, range(L), [ctx - 1])
+    out = torch.empty((L, 1, m, d), dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    _, ws_bytes = d200.query_sizes(cfg)
+    for deep in (0, 1):
+        print("max active clusters (deep=%d):" % deep,
+              {cs: lib.delta_debug_cluster_occupancy(deep, cs) for cs in (2, 4, 8, 12, 16)})
+    tunes = os.environ.get("PROBE_TUNES", "auto").split(";")
+    for tune in tunes:
+        if tune == "auto":
+            os.environ.pop("DELTA_TUNE", None)
+        else:
+            os.environ["DELTA_TUNE"] = tune
+        st = d200.DeltaStack(cfg, base.kv_pool, base.block_table,
+                             torch.zeros(ws_bytes, dtype=torch.uint8, device="cuda"))
+        st.set_seq_lens([ctx - 1])
+        with torch.cuda.stream(s):
+            st.decode_step(q, k, v, out, stream=s)
+        s.synchronize()
+        read()
+        print(f"########## tune: {tune}")
+        for name, fn in (("FULL layer 0", lambda: st.decode_layer(0, q[0], out[0], stream=s)),
+                         ("SPARSE layer 3", lambda: st.decode_layer(3, q[3], out[3], stream=s))):
+            for rep in range(2):
+                with torch.cuda.stream(s):
+                    fn()
+                s.synchronize()
+                report(f"{name} rep {rep}", read())
+        # back-to-back: the step's own sequence, eager (timed with events too)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with torch.cuda.stream(s):
+            ev[0].record(s)
+            for l in range(3, 16):
+                st.decode_layer(l, q[l], out[l], stream=s)
+            ev[1].record(s)
+        s.synchronize()
+        report(f"SPARSE layer 15 after 3..14 back to back ({ev[0].elapsed_time(ev[1]) * 1e3 / 13:.2f} us/layer)",
+               read())
+        assert st.get_error() == 0
+        st.set_seq_lens([ctx - 1])
+        reps = 20
+        with torch.cuda.stream(s):
+            st.decode_step(q, k, v, out, stream=s)
+            s.synchronize()
+            for _ in range(3):
+                st.set_seq_lens([ctx - 1])
+            ev[0].record(s)
+            for _ in range(reps):
+                st.decode_layer(0, q[0], out[0], stream=s)
+            ev[1].record(s)
+        s.synchronize()
+        print(f"   FULL layer eager back-to-back: {ev[0].elapsed_time(ev[1]) * 1e3 / reps:.2f} us")
+        read()
+
+
+if __name__ == "__main__":
+    main()
