@@ -10,6 +10,7 @@ namespace {
 __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
     const int b = blockIdx.x;
     pdl_wait();
+    pdl_launch_dependents();
     const int n = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
     if (n + p.ntok > p.max_seq) {
         if (threadIdx.x == 0) set_err(p.err, kDevCapacity);
@@ -35,7 +36,6 @@ __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
             *reinterpret_cast<const uint4*>(vs + src_off);
     }
     __syncthreads();
-    pdl_launch_dependents();
     if (threadIdx.x == 0) p.seq_len[p.layer * p.max_batch + b] = (n + p.ntok) * p.g;
 }
 

@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(NW * 32) attn_simt_kernel(const AttnParams p) 
     const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int gs = p.gs;
     pdl_wait();
+    pdl_launch_dependents();  // after the wait: the next kernel may launch (see attn_tc.cu)
 
     const int n_old = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
     const int s = p.fuse_append ? n_old + 1 : n_old;
@@ -137,7 +138,6 @@ __global__ void __launch_bounds__(NW * 32) attn_simt_kernel(const AttnParams p) 
         for (int v = 0; v < VPL; ++v) os[(warp * 16 + j) * os_stride<D>() + lane * VPL + v] = o[j][v];
     }
     __syncthreads();
-    pdl_launch_dependents();
     cluster_epilogue<D, NW>(p, ms, ls, os, cstage, b, h, stale, cap_err, s);
 }
 

@@ -41,18 +41,23 @@ extern "C" int delta_trace_read(void* host, size_t bytes) {  // copies then clea
 namespace delta {
 namespace {
 
-constexpr int NCW = 4;      // consumer warps
+constexpr int NT = 3;            // tiles per ring stage
+constexpr int NGRP = 2;          // consumer groups; ring slot i is always consumed by group i % NGRP
+constexpr int NCW = NT * NGRP;   // consumer warps (more than one per SM sub-partition: latency hiding)
+constexpr int kBatch = (32 / NT) * NT;  // tiles whose page ids the producer resolves at once
 constexpr int kThreads = (NCW + 1) * 32;
-// pipeline depth (stages of NCW head-pages): kDeep when one CTA per SM (few CTAs, e.g. batch
-// 1), kShallow when two CTAs share an SM.
-constexpr int kDeep = 6, kShallow = 3;
+// pipeline depth in stages of NT head-pages: kDeep when one CTA per SM, kShallow when two CTAs
+// share an SM.  Must be a multiple of NGRP: a group then always consumes the same slots, in
+// consecutive rounds, so its mbarrier parity waits can never alias a round it skipped.
+constexpr int kDeep = 8, kShallow = 4;
+static_assert(kDeep % NGRP == 0 && kShallow % NGRP == 0, "ring slots must map to fixed consumer groups");
 
 template <int D, int NSTAGE>
 struct TcCfg {
     static constexpr int kHalf = kPage * D * 2;        // bytes of one head-page of K (or of V)
     static constexpr int kTile = 2 * kHalf;            // K then V of one (page, head): one TMA request
-    static constexpr int kRing = NSTAGE * NCW * kTile;
-    static constexpr int kRowTok = NSTAGE * NCW * kPage;  // token id of every ring row (-1 = none)
+    static constexpr int kRing = NSTAGE * NT * kTile;
+    static constexpr int kRowTok = NSTAGE * NT * kPage;  // token id of every ring row (-1 = none)
     static constexpr int kSmem = 1024 + kRing + ClusterStage<D>::kBytes + 2 * NSTAGE * 8 + kRowTok * 4 + 16;
 };
 
@@ -68,16 +73,16 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 }
 
 template <int D, bool TOKEN_PLAN, int NSTAGE, int NH>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, NH == 1 ? 2 : 1)  // two CTAs per SM (cluster residency)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     using C = TcCfg<D, NSTAGE>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* ring = base;  // [NSTAGE][NCW] tiles of kTile bytes: K rows then V rows
+    uint8_t* ring = base;  // [NSTAGE][NT] tiles of kTile bytes: K rows then V rows
     float* cstage = reinterpret_cast<float*>(ring + C::kRing);  // peers push partials here
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + C::kRing + ClusterStage<D>::kBytes);
     uint64_t* empty = full + NSTAGE;
-    int* rowtok = reinterpret_cast<int*>(empty + NSTAGE);  // [NSTAGE][NCW][P], written by the producer
+    int* rowtok = reinterpret_cast<int*>(empty + NSTAGE);  // [NSTAGE][NT][P], written by the producer
     int* sflag = rowtok + C::kRowTok;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -86,7 +91,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     if (tid == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
             mbar_init(&full[i], TOKEN_PLAN ? 32 : 1);
-            mbar_init(&empty[i], NCW);
+            mbar_init(&empty[i], NT);
         }
         fence_mbar_init();
     }
@@ -128,6 +133,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     const int32_t* plan_phys = p.plan_phys + (size_t)b * p.plan_cap;
     const size_t layer_ph = (size_t)p.layer * p.num_phys;
     if (p.prewait && warp != NCW) pdl_wait();
+    // Every CTA has passed its wait here (the producer never reads upstream outputs), so the
+    // previous kernel is complete: let the next layer's kernel launch now — its CTAs co-reside
+    // (two per SM), resolve their geometry and start their KV stream during this kernel.
+    if (p.early_trigger && warp == 0) pdl_launch_dependents();
     const __nv_bfloat16* k_new = reinterpret_cast<const __nv_bfloat16*>(p.k_new) + ((size_t)b * p.g + h) * D;
     const __nv_bfloat16* v_new = reinterpret_cast<const __nv_bfloat16*>(p.v_new) + ((size_t)b * p.g + h) * D;
 
@@ -159,41 +168,48 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
         // L2 round trips per batch rather than per tile.  The token id of every ring row is
         // handed to the consumers through shared memory (published by the stage barrier).
         if (!TOKEN_PLAN) {
-            for (int base = 0; base < n_items; base += 32) {
-                int my_lp = -1, my_phys = 0;
-                if (base + lane < n_items) {
+            // page ids of one batch of tiles (lane i: tile base + i)
+            auto resolve = [&](int base, int& lp, int& phys) {
+                lp = -1;
+                phys = 0;
+                if (lane < kBatch && base + lane < n_items) {
                     if (p.role == kRoleSparse) {  // logical and physical page: independent loads
-                        my_lp = plan[unit0 + base + lane];
-                        my_phys = plan_phys[unit0 + base + lane];
+                        lp = plan[unit0 + base + lane];
+                        phys = plan_phys[unit0 + base + lane];
                     } else {
-                        my_lp = unit0 + base + lane;
-                        my_phys = bt[my_lp];
+                        lp = unit0 + base + lane;
+                        phys = bt[lp];
                     }
                 }
-                const int nb = min(32, n_items - base);
-                for (int j = 0; j < nb; j += NCW) {
-                    const int iter = (base + j) / NCW;
+            };
+            int my_lp, my_phys;
+            resolve(0, my_lp, my_phys);
+            for (int base = 0; base < n_items; base += kBatch) {
+                if (base > 0) resolve(base, my_lp, my_phys);
+                const int nb = min(kBatch, n_items - base);
+                for (int j = 0; j < nb; j += NT) {
+                    const int iter = (base + j) / NT;
                     const int stg = iter % NSTAGE, round = iter / NSTAGE;
                     if (round > 0) mbar_wait(&empty[stg], (round - 1) & 1);
-                    const int valid = min(NCW, nb - j);
+                    const int valid = min(NT, nb - j);
 #pragma unroll
-                    for (int k = 0; k < (NCW * kPage) / 32; ++k) {
+                    for (int k = 0; k < (NT * kPage + 31) / 32; ++k) {
                         const int rr = lane + 32 * k, w = rr / kPage, r = rr % kPage;
-                        const int lp_w = __shfl_sync(0xffffffffu, my_lp, j + w);
+                        const int lp_w = __shfl_sync(0xffffffffu, my_lp, min(j + w, 31));
                         int t = -1;
                         if (w < valid) {
                             t = lp_w * kPage + r;
                             if (t >= s) t = -1;
                         }
-                        rowtok[(stg * NCW + w) * kPage + r] = t;
+                        if (rr < NT * kPage) rowtok[(stg * NT + w) * kPage + r] = t;
                     }
-                    const int phys_w = __shfl_sync(0xffffffffu, my_phys, j + (lane % NCW));
+                    const int phys_w = __shfl_sync(0xffffffffu, my_phys, j + (lane % NT));
                     __syncwarp();
                     if (lane == 0) mbar_arrive_expect_tx(&full[stg], valid * C::kTile);
                     __syncwarp();
                     if (lane < valid) {  // one 2P-row box: this head's K and V rows of the page
                         const int row0 = (int)kv_row(layer_ph + phys_w, p.g, h, 0);
-                        uint8_t* dst = ring + (stg * NCW + lane) * C::kTile;
+                        uint8_t* dst = ring + (stg * NT + lane) * C::kTile;
                         if (D == 64) tma_load_2d(dst, &tm_kv, &full[stg], 0, row0, kEvictFirst);
                         else tma_load_3d(dst, &tm_kv, &full[stg], 0, 0, row0, kEvictFirst);
                     }
@@ -202,34 +218,39 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
         } else {
             const __nv_bfloat16* pool = reinterpret_cast<const __nv_bfloat16*>(p.kv_pool);
             constexpr int kChunks = D / 8;
-            constexpr int kRowsPerStage = NCW * kPage;  // 64
-            for (int it = 0, iter = 0; it < n_items; it += NCW, ++iter) {
+            constexpr int kRowsPerStage = NT * kPage;
+            constexpr int kRowIt = (kRowsPerStage + 31) / 32;  // rows per lane
+            for (int it = 0, iter = 0; it < n_items; it += NT, ++iter) {
                 const int stg = iter % NSTAGE, round = iter / NSTAGE;
-                // resolve the stage's rows: lane owns rows lane and lane + 32 (token -> pool row)
-                long long my_row[kRowsPerStage / 32];
-                int my_t[kRowsPerStage / 32];
+                // resolve the stage's rows: lane owns rows lane + 32k (token -> pool row)
+                long long my_row[kRowIt];
+                int my_t[kRowIt];
 #pragma unroll
-                for (int k = 0; k < kRowsPerStage / 32; ++k) {  // token and its physical slot: independent
+                for (int k = 0; k < kRowIt; ++k) {  // token and its physical slot: independent loads
                     const int rr = lane + 32 * k, w = rr / kPage, r = rr % kPage;
                     const int e = unit0 + (it + w) * kPage + r;
-                    const bool ok = it + w < n_items && e < e_end;
+                    const bool ok = rr < kRowsPerStage && it + w < n_items && e < e_end;
                     my_t[k] = ok ? plan[e] : -1;
                     const int ps = ok ? plan_phys[e] : 0;  // phys_page * P + slot
                     my_row[k] = ok ? (long long)kv_row(layer_ph + ps / kPage, p.g, h, ps % kPage) : -1ll;
                 }
                 if (round > 0) mbar_wait(&empty[stg], (round - 1) & 1);
 #pragma unroll
-                for (int k = 0; k < kRowsPerStage / 32; ++k) rowtok[stg * kRowsPerStage + lane + 32 * k] = my_t[k];
-                for (int w = 0; w < NCW; ++w) {
+                for (int k = 0; k < kRowIt; ++k)
+                    if (lane + 32 * k < kRowsPerStage) rowtok[stg * kRowsPerStage + lane + 32 * k] = my_t[k];
+                for (int w = 0; w < NT; ++w) {
                     if (it + w >= n_items) break;
-                    uint8_t* kd = ring + (stg * NCW + w) * C::kTile;
+                    uint8_t* kd = ring + (stg * NT + w) * C::kTile;
                     uint8_t* vd = kd + C::kHalf;
                     for (int ci = lane; ci < kPage * kChunks; ci += 32) {
                         const int r = ci / kChunks, c = ci - r * kChunks;
                         const int rr = w * kPage + r;
-                        const long long r0 = __shfl_sync(0xffffffffu, my_row[0], rr & 31);
-                        const long long r1 = __shfl_sync(0xffffffffu, my_row[1], rr & 31);
-                        const long long row = (rr >> 5) ? r1 : r0;
+                        long long row = -1;
+#pragma unroll
+                        for (int k = 0; k < kRowIt; ++k) {
+                            const long long x = __shfl_sync(0xffffffffu, my_row[k], rr & 31);
+                            if ((rr >> 5) == k) row = x;
+                        }
                         if (row >= 0) {
                             cp_async16(kd + swz<D>(r, c), pool + row * D + c * 8);
                             cp_async16(vd + swz<D>(r, c), pool + (row + kPage) * D + c * 8);
@@ -278,15 +299,17 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
         }
         const float sl2 = p.scale_log2;
 
-        for (int it = 0, iter = 0; it < n_items; it += NCW, ++iter) {
+        const int grp = warp / NT, wt = warp % NT;  // consumer group, tile within the stage
+        for (int iter = grp; iter * NT < n_items; iter += NGRP) {
+            const int it = iter * NT;
             const int stg = iter % NSTAGE, round = iter / NSTAGE;
             mbar_wait(&full[stg], round & 1);
             if (iter == 0 && tid == 0) DTRACE(2);
-            const int item = it + warp;
+            const int item = it + wt;
             if (item < n_items) {
-                uint8_t* kt = ring + (stg * NCW + warp) * C::kTile;
+                uint8_t* kt = ring + (stg * NT + wt) * C::kTile;
                 uint8_t* vt = kt + C::kHalf;
-                const int* rt = rowtok + (stg * NCW + warp) * kPage;
+                const int* rt = rowtok + (stg * NT + wt) * kPage;
                 const int my_tok = (lane < kPage) ? rt[lane] : -1;  // token of ring row `lane`
                 const int tok0 = rt[g4], tok1 = rt[g4 + 8];         // tokens of this lane's S^T rows
                 // fused append: patch row holding token s-1 from the inputs
@@ -315,6 +338,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
                 }
                 __syncwarp();
                 const uint32_t kt_u = smem_u32(kt), vt_u = smem_u32(vt);
+                {
                 // ---- S^T = K Q^T: two accumulator chains (even / odd k-chunks)
                 float acc[NH][4], acc2[NH][4];
 #pragma unroll
@@ -351,29 +375,51 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
                             if (hq < gs && t >= 0) lg[(size_t)t * p.m + hq] = c[i] * p.scale;
                         }
                     }
-                    // ---- online softmax per head column (log2 domain)
-                    float pr[4];
+                    // ---- softmax per head column (log2 domain) with a lazily raised stabiliser:
+                    // p = exp2(x - m) for ANY m gives the same normalised softmax (the
+                    // epilogue divides by the same sums), so m is only moved -- with the
+                    // cross-lane max and the rescale of O -- when a logit exceeds it by more
+                    // than kHeadroom (p then stays <= 2^kHeadroom, far inside fp32/bf16
+                    // range; logits far below m underflow only below 2^-126 relative).
+                    // The first valid tile of a warp always sets m.  Deterministic: m depends
+                    // only on the data, in a fixed order.
+                    constexpr float kHeadroom = 16.f;
+                    float x[4];
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        const float x0 = tok0 >= 0 ? c[e] * sl2 : -INFINITY;
-                        const float x1 = tok1 >= 0 ? c[2 + e] * sl2 : -INFINITY;
-                        float mx = fmaxf(x0, x1);
-                        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-                        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-                        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-                        const float mn = fmaxf(mh[nh][e], mx);
-                        const float msafe = (mn == -INFINITY) ? 0.f : mn;
-                        const float al = ex2(mh[nh][e] - msafe);
-                        pr[e] = ex2(x0 - msafe);
-                        pr[2 + e] = ex2(x1 - msafe);
-                        lh[nh][e] = lh[nh][e] * al + (pr[e] + pr[2 + e]);
-                        mh[nh][e] = mn;
+                        x[e] = tok0 >= 0 ? c[e] * sl2 : -INFINITY;
+                        x[2 + e] = tok1 >= 0 ? c[2 + e] * sl2 : -INFINITY;
+                    }
+                    const bool raise = fmaxf(x[0], x[2]) > mh[nh][0] + kHeadroom ||
+                                       fmaxf(x[1], x[3]) > mh[nh][1] + kHeadroom;
+                    if (__any_sync(0xffffffffu, raise)) {  // rare after the first tile
 #pragma unroll
-                        for (int mt = 0; mt < D / 16; ++mt) {
-                            o[nh][mt][e] *= al;
-                            o[nh][mt][2 + e] *= al;
+                        for (int e = 0; e < 2; ++e) {
+                            float mx = fmaxf(x[e], x[2 + e]);
+                            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+                            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+                            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+                            const float mn = fmaxf(mh[nh][e], mx);
+                            if (mn > mh[nh][e]) {
+                                const float al = ex2(mh[nh][e] - mn);  // mh = -inf -> 0
+                                lh[nh][e] *= al;
+#pragma unroll
+                                for (int mt = 0; mt < D / 16; ++mt) {
+                                    o[nh][mt][e] *= al;
+                                    o[nh][mt][2 + e] *= al;
+                                }
+                                mh[nh][e] = mn;
+                            }
                         }
                     }
+                    float pr[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {  // x = -inf -> 0 (m = -inf only while every x is -inf)
+                        const float m = mh[nh][i & 1];
+                        pr[i] = ex2(x[i] - (m == -INFINITY ? 0.f : m));
+                    }
+                    lh[nh][0] += pr[0] + pr[2];
+                    lh[nh][1] += pr[1] + pr[3];
                     // ---- P^T operand: bf16 hi + lo (P keeps ~16 mantissa bits), transposed
                     const __nv_bfloat162 h01 = __floats2bfloat162_rn(pr[0], pr[1]);
                     const __nv_bfloat162 h23 = __floats2bfloat162_rn(pr[2], pr[3]);
@@ -384,8 +430,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
                     blo[nh][1] = movmatrix_trans(pack_bf16(pr[2] - f23.x, pr[3] - f23.y));
                 }
                 // ---- O^T += V^T P^T
+                constexpr int kPvTiles = D / 16;
 #pragma unroll
-                for (int mt = 0; mt < D / 16; ++mt) {
+                for (int mt = 0; mt < kPvTiles; ++mt) {
                     uint32_t a0, a1, a2, a3;
                     ldsm_x4_t(vt_u + swz<D>((lane & 7) + 8 * (lane >> 4), mt * 2 + ((lane >> 3) & 1)), a0, a1, a2, a3);
                     const uint32_t af[4] = {a0, a1, a2, a3};
@@ -396,6 +443,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
                             mma_bf16_16816(o[nh][mt], af, blo[nh][0], blo[nh][1]);
                         }
                     }
+                }
                 }
                 // generic-proxy smem writes must be ordered before the next TMA refill
                 if (wrote_smem) fence_proxy_async_smem();
@@ -433,7 +481,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
         }
     }
     __syncthreads();  // producer joins: warp states complete
-    pdl_launch_dependents();
+    if (!p.early_trigger) pdl_launch_dependents();
     if (tid == 0) DTRACE(4);
     cluster_epilogue<D, NCW>(p, ms, ls, os, cstage, b, h, stale, cap_err, s);
     if (tid == 0) DTRACE(6);

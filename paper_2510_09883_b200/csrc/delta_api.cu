@@ -197,6 +197,7 @@ struct delta_ctx {
     uint64_t launches = 0;
     bool pdl = true;
     int tune_nsplit = 0, tune_deep = -1;  // DELTA_TUNE overrides (0 / -1 = automatic)
+    int tune_prewait = 1, tune_early = 1;
     // the previous kernel this handle enqueued (decides whether the next attention kernel
     // may start its KV stream before griddepcontrol.wait; see attn_tc.cu)
     enum { kLastNone, kLastAttn, kLastSelect, kLastAppend } last_kind = kLastNone;
@@ -268,7 +269,7 @@ delta_status check_sparse_fresh(delta_ctx* h, int layer, bool appending) {
 }
 
 delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new, const void* v_new,
-                           const void* q, float* out, float* lse_out, cudaStream_t st) {
+                           const void* q, float* out, float* lse_out, cudaStream_t st, bool in_step = false) {
     AttnParams p = attn_params(h, layer, batch);
     p.q = q; p.out = out; p.lse_out = lse_out;
     p.fuse_append = (k_new != nullptr);
@@ -276,7 +277,11 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
     // May the kernel read its length counter, block table and plan before the previous kernel
     // completes?  Not if that kernel is this layer's own (append / attention: the counter) or
     // the select that wrote this sparse layer's plan.
-    p.prewait = 1;
+    // Only inside a captured step, where every kernel on the stream is this handle's and in
+    // this order; eager calls may follow other work on the stream.
+    p.prewait = (in_step && h->tune_prewait) ? 1 : 0;
+    p.early_trigger = h->tune_early;
+    if (h->last_kind == delta_ctx::kLastNone) p.prewait = 0;
     if (h->last_layer == layer && (h->last_kind == delta_ctx::kLastAppend || h->last_kind == delta_ctx::kLastAttn))
         p.prewait = 0;
     if (p.role == kRoleSparse && h->last_kind == delta_ctx::kLastSelect && h->last_layer == h->gov[layer])
@@ -330,8 +335,9 @@ delta_status enqueue_step(delta_ctx* h, int batch, const void* q_all, const void
         const uint8_t* q = static_cast<const uint8_t*>(q_all) + l * q_l * e;
         const uint8_t* k = static_cast<const uint8_t*>(k_all) + l * kv_l * e;
         const uint8_t* v = static_cast<const uint8_t*>(v_all) + l * kv_l * e;
+        if (l == 0) h->last_kind = delta_ctx::kLastNone;  // first node: its predecessor is outside the step
         delta_status s = launch_decode(h, l, batch, k, v, q, out_all + l * q_l,
-                                       lse_all ? lse_all + (size_t)l * batch * c.num_q_heads : nullptr, st);
+                                       lse_all ? lse_all + (size_t)l * batch * c.num_q_heads : nullptr, st, true);
         if (s != DELTA_OK) return s;
         if (h->role[l] == kRoleSelect) {
             s = launch_sel(h, l, batch, nullptr, nullptr, nullptr, st);
@@ -449,6 +455,8 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
         const char* d = std::strstr(t, "deep=");
         if (a) h->tune_nsplit = std::atoi(a + 7);
         if (d) h->tune_deep = std::atoi(d + 5);
+        if (const char* w = std::strstr(t, "prewait=")) h->tune_prewait = std::atoi(w + 8);
+        if (const char* w = std::strstr(t, "early=")) h->tune_early = std::atoi(w + 6);
     }
     h->step.assign(cfg->num_layers, 0);
     h->dec_step.assign(cfg->num_layers, -1);

@@ -34,6 +34,7 @@ struct AttnParams {
     int fuse_append;    // 1: append k_new/v_new at position seq_len (pre) in this launch
     int deep;           // 1: one CTA per SM with the deep TMA ring (few CTAs), 0: shallow ring
     int prewait;        // 1: start geometry + KV stream before griddepcontrol.wait (see attn_tc.cu)
+    int early_trigger;  // 1: launch_dependents right after the wait (else after the main loop)
     float scale;        // softmax scale (natural units)
     float scale_log2;   // scale * log2(e)
     const void* q;      // [batch][m][d]

@@ -7,16 +7,20 @@
 #include <stdint.h>
 
 #ifdef DELTA_TRACE
-// Phase timestamps (%globaltimer, ns) per CTA for latency analysis; trace builds only
-// (`make trace`), never the product library.
-static __device__ unsigned long long g_delta_trace[8192 * 12];
+// Phase timestamps (%globaltimer, ns) per (layer, CTA) for latency analysis; trace builds
+// only (`make trace`), never the product library.  Uses `p.layer` of the enclosing kernel.
+static __device__ unsigned long long g_delta_trace[64 * 512 * 12];
 #define DTRACE(slot)                                                                          \
     do {                                                                                      \
         unsigned long long t_;                                                                \
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                \
         const unsigned cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
-        if (cta_ < 8192) g_delta_trace[cta_ * 12 + (slot)] = t_;                               \
+        if (cta_ < 512 && (p.layer + DTRACE_LAYER_OFF) < 64)                                   \
+            g_delta_trace[((p.layer + DTRACE_LAYER_OFF) * 512 + cta_) * 12 + (slot)] = t_;      \
     } while (0)
+#ifndef DTRACE_LAYER_OFF
+#define DTRACE_LAYER_OFF 0
+#endif
 #else
 #define DTRACE(slot) do {} while (0)
 #endif

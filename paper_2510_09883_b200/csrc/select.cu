@@ -13,6 +13,7 @@
 //   k by (key desc, index asc) (R9) — compacted in ascending unit order with block scans.
 // Integer radix + fixed-order float sums: deterministic, bit-exact to any correct top-k on
 // the same fp32 key buffer.
+#define DTRACE_LAYER_OFF 32  // trace builds: select stamps go to layer slot + 32
 #include "combine.cuh"
 
 namespace delta {
@@ -57,10 +58,15 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scratch, int* total) 
 }
 
 // max_j (a_j(t) - LSE_j) over the heads j this lane owns: lane pair (hh = 0, 1) splits the m
-// heads of token t.  m % 4 == 0: 16-byte loads, all issued before the max chain (the row is
-// 16-byte aligned because the logits are [s][m] fp32).  Max is exact, so the split and the
-// order do not change the result.
-__device__ __forceinline__ float head_max(const float* __restrict__ row, const float* lse_s, int m, int hh) {
+// heads of token t; lane hh owns the 16-byte head groups q = hh, hh+2, ... (m % 4 == 0; the
+// row is 16-byte aligned because the logits are [s][m] fp32).  `lse4` holds this lane's LSE
+// groups in registers.  Max is exact, so the split and the order do not change the result.
+struct LseLane {
+    float4 v[8];  // q = hh + 2i, i < 8 (m <= 64); larger m falls back to global loads
+};
+
+__device__ __forceinline__ float head_max(const float* __restrict__ row, const LseLane& ls,
+                                          const float* __restrict__ lse_g, int m, int hh) {
     float mx = -INFINITY;
     if ((m & 3) == 0) {
         const float4* r4 = reinterpret_cast<const float4*>(row);
@@ -75,32 +81,35 @@ __device__ __forceinline__ float head_max(const float* __restrict__ row, const f
         for (int i = 0; i < 8; ++i) {
             const int q = hh + 2 * i;
             if (q < n4) {
-                mx = fmaxf(mx, fmaxf(fmaxf(v[i].x - lse_s[4 * q], v[i].y - lse_s[4 * q + 1]),
-                                     fmaxf(v[i].z - lse_s[4 * q + 2], v[i].w - lse_s[4 * q + 3])));
+                const float4 l = ls.v[i];
+                mx = fmaxf(mx, fmaxf(fmaxf(v[i].x - l.x, v[i].y - l.y), fmaxf(v[i].z - l.z, v[i].w - l.w)));
             }
         }
+        const float4* l4 = reinterpret_cast<const float4*>(lse_g);
         for (int q = hh + 16; q < n4; q += 2) {
-            const float4 w = r4[q];
-            mx = fmaxf(mx, fmaxf(fmaxf(w.x - lse_s[4 * q], w.y - lse_s[4 * q + 1]),
-                                 fmaxf(w.z - lse_s[4 * q + 2], w.w - lse_s[4 * q + 3])));
+            const float4 w = r4[q], l = l4[q];
+            mx = fmaxf(mx, fmaxf(fmaxf(w.x - l.x, w.y - l.y), fmaxf(w.z - l.z, w.w - l.w)));
         }
     } else {
 #pragma unroll 8
-        for (int j = hh; j < m; j += 2) mx = fmaxf(mx, row[j] - lse_s[j]);
+        for (int j = hh; j < m; j += 2) mx = fmaxf(mx, row[j] - lse_g[j]);
     }
     return mx;
 }
 
 __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams p) {
     extern __shared__ uint32_t sm_keys[];  // [kSmemUnits] (only when it fits)
-    __shared__ float lse_s[256];
     __shared__ int scratch[kSelWarps + 1];
     __shared__ int hist[256];
+    __shared__ int whist[kSelWarps * 256];
     __shared__ int s_flag, s_bin, s_rem;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int b = blockIdx.y;
+    if (tid == 0) DTRACE(0);
     pdl_wait();
+    pdl_launch_dependents();  // the next kernel's reads of this plan come after its own wait
+    if (tid == 0) DTRACE(1);
 
     const int s = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
     const int block = p.sel_block;
@@ -110,8 +119,17 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
 
     // ------------------------------------------------------------ phase A: scores
     if (!p.keys_override) {
-        for (int j = tid; j < p.m; j += kSelThreads) lse_s[j] = p.lse_buf[(size_t)b * p.m + j];
-        __syncthreads();
+        const float* lse_g = p.lse_buf + (size_t)b * p.m;
+        LseLane lsl;
+        {
+            const int hh0 = lane & 1, n4 = p.m >> 2;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int q = hh0 + 2 * i;
+                lsl.v[i] = ((p.m & 3) == 0 && q < n4) ? reinterpret_cast<const float4*>(lse_g)[q]
+                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
         const int per = (n_units + p.nchunk - 1) / p.nchunk;
         const int u_lo = blockIdx.x * per, u_hi = min(n_units, u_lo + per);
         const float* lg = p.logits + (size_t)b * p.max_seq * p.m;
@@ -121,7 +139,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
             for (int u = u_lo + warp; u < u_hi; u += kSelWarps) {
                 const int t = u * kPage + jr;
                 float mx = -INFINITY;
-                if (t < s) mx = head_max(lg + (size_t)t * p.m, lse_s, p.m, hh);
+                if (t < s) mx = head_max(lg + (size_t)t * p.m, lsl, lse_g, p.m, hh);
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
                 const float e = (t < s) ? expf(mx) : 0.f;
                 float sum = 0.f;
@@ -134,20 +152,21 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
             for (int t0 = t_lo + warp * 16; t0 < t_hi; t0 += kSelWarps * 16) {
                 const int t = t0 + jr;
                 float mx = -INFINITY;
-                if (t < t_hi) mx = head_max(lg + (size_t)t * p.m, lse_s, p.m, hh);
+                if (t < t_hi) mx = head_max(lg + (size_t)t * p.m, lsl, lse_g, p.m, hh);
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
                 if (t < t_hi && hh == 0) keys_b[t] = mx;
             }
         }
         __threadfence();
         __syncthreads();
+        if (tid == 0) DTRACE(2);
         if (tid == 0) s_flag = (atomicAdd(&p.cnt[b], 1) == p.nchunk - 1);
         __syncthreads();
         if (!s_flag) return;
+        if (tid == 0) DTRACE(3);
         __threadfence();
         if (tid == 0) p.cnt[b] = 0;
     }
-    pdl_launch_dependents();
 
     // ------------------------------------------------------------ phase B: top-k
     int32_t* plan = p.plan_idx + (size_t)b * p.plan_cap;
@@ -185,17 +204,28 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
         __syncthreads();
         auto K = [&](int u) -> uint32_t { return cached ? sm_keys[u] : key_bits(__ldcg(src + u)); };
 
+        if (tid == 0) DTRACE(6);
         uint32_t prefix = 0, maskbits = 0;
         int remaining = p.k_units;
         if (remaining > 0) {
             for (int pass = 0; pass < 4; ++pass) {
                 const int shift = 24 - 8 * pass;
-                if (tid < 256) hist[tid] = 0;
+                // per-warp private histograms: the keys share their top digits, so a shared
+                // histogram would serialise every warp on the same bins
+                for (int i = tid; i < kSelWarps * 256; i += kSelThreads) whist[i] = 0;
                 __syncthreads();
+                int* myh = whist + warp * 256;
                 for (int u = tid; u < n_units; u += kSelThreads) {
                     if (forced(u)) continue;
                     const uint32_t v = K(u);
-                    if ((v & maskbits) == prefix) atomicAdd(&hist[(v >> shift) & 255], 1);
+                    if ((v & maskbits) == prefix) atomicAdd(&myh[(v >> shift) & 255], 1);
+                }
+                __syncthreads();
+                if (tid < 256) {
+                    int c = 0;
+#pragma unroll
+                    for (int w = 0; w < kSelWarps; ++w) c += whist[w * 256 + tid];
+                    hist[tid] = c;
                 }
                 __syncthreads();
                 if (warp == 0) {  // one warp walks the 256 bins in descending order
@@ -228,8 +258,10 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
                 prefix |= (uint32_t)s_bin << shift;
                 maskbits |= 0xFFu << shift;
                 remaining = s_rem;
+                if (tid == 0) DTRACE(7 + pass);
             }
         }
+        if (tid == 0) DTRACE(4);
         const uint32_t T = prefix;
         const int need_eq = remaining;  // keys equal to T still to take (lowest index first)
         const bool take_any = p.k_units > 0;
@@ -237,6 +269,16 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
         int carry_eq = 0, carry_pos = 0;
         for (int base = 0; base < n_units; base += kSelThreads * IPT) {
             const int u0 = base + tid * IPT;
+            // physical locations of this thread's units, loaded before the scans (overlap)
+            int32_t phys[IPT];
+            if (block == 1) {
+                const int32_t pg = u0 < n_units ? bt[u0 / kPage] : 0;  // u0..u0+7 share a page
+#pragma unroll
+                for (int i = 0; i < IPT; ++i) phys[i] = pg * kPage + ((u0 + i) % kPage);
+            } else {
+#pragma unroll
+                for (int i = 0; i < IPT; ++i) phys[i] = (u0 + i < n_units) ? bt[u0 + i] : 0;
+            }
             uint32_t fl_f = 0, fl_gt = 0, fl_eq = 0;  // bit i: unit u0 + i is forced / > T / == T
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
@@ -267,7 +309,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
                 if (fl_sel & (1u << i)) {
                     if (pos < p.plan_cap) {
                         plan[pos] = u0 + i;
-                        plan_phys[pos] = phys_of(u0 + i);
+                        plan_phys[pos] = phys[i];
                     }
                     ++pos;
                 }
@@ -279,6 +321,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
         if (count > p.plan_cap) set_err(p.err, kDevUsage);
     }
     __syncthreads();
+    if (tid == 0) DTRACE(5);
     if (tid == 0) {
         p.plan_count[b] = min(count, p.plan_cap);
         p.plan_stamp[b] = s;
@@ -292,6 +335,18 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
 }
 
 }  // namespace
+
+#ifdef DELTA_TRACE
+extern "C" int delta_trace_read_select(void* host, size_t bytes) {  // this TU's copy of the stamps
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess)
+        e = cudaMemcpyFromSymbol(host, g_delta_trace, bytes < sizeof(g_delta_trace) ? bytes : sizeof(g_delta_trace));
+    void* dev = nullptr;
+    if (e == cudaSuccess) e = cudaGetSymbolAddress(&dev, g_delta_trace);
+    if (e == cudaSuccess) e = cudaMemset(dev, 0, sizeof(g_delta_trace));
+    return (int)e;
+}
+#endif
 
 size_t select_smem_bytes(int max_units) {
     return (size_t)min(max_units, kSmemUnits) * sizeof(uint32_t);

@@ -18,15 +18,22 @@ import synth  # noqa: E402
 from synth import device as sd  # noqa: E402
 
 lib = d200.load_library()
-buf = np.zeros(8192 * 12, np.uint64)
+buf = np.zeros(64 * 512 * 12, np.uint64)
+
+
+buf2 = np.zeros(64 * 512 * 12, np.uint64)
 
 
 def read():
     assert lib.delta_trace_read(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes)) == 0
-    return buf.reshape(8192, 12).astype(np.int64).copy()
+    assert lib.delta_trace_read_select(buf2.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf2.nbytes)) == 0
+    a = buf.reshape(64, 512, 12).astype(np.int64)
+    a[32:] = buf2.reshape(64, 512, 12).astype(np.int64)[32:]
+    return a.copy()
 
 
-def report(name, tr):
+def report(name, tr3):
+    tr = tr3.reshape(-1, 12)
     live = tr[:, 0] > 0
     t = tr[live]
     t0 = t[:, 0].min()
@@ -108,6 +115,38 @@ def main():
         s.synchronize()
         print(f"   FULL layer eager back-to-back: {ev[0].elapsed_time(ev[1]) * 1e3 / reps:.2f} us")
         read()
+        # graph-captured step (prewait + early trigger): per-layer timeline of the last replay
+        st.set_seq_lens([ctx - 1])
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                st.set_seq_lens([ctx - 1])
+                st.decode_step(q, k, v, out, stream=s)
+        s.synchronize()
+        tr = read()
+        t0 = tr[:, :, 0][tr[:, :, 0] > 0].min()
+        print("   graph step timeline (us from first CTA entry):  layer: entry_min pdl_med data_med loop_med "
+              "loop_max push_med sync_med sync_max out_max epi_end")
+        for l in list(range(L)) + [32 + d for d in delta]:
+            if l >= 32:
+                t = tr[l]
+                live = t[:, 0] > 0
+                if live.any():
+                    t = t[live]
+                    g = lambda k, fn: (fn(t[:, k][t[:, k] > 0]) - t0) / 1e3 if (t[:, k] > 0).any() else float("nan")
+                    print(f"   select L{l - 32}: entry {g(0, np.min):7.2f} waited {g(1, np.max):7.2f} phaseA_done "
+                          f"{g(2, np.max):7.2f} elected {g(3, np.max):7.2f} radix_done {g(4, np.max):7.2f} "
+                          f"plan_done {g(5, np.max):7.2f} | keys {g(6, np.max):7.2f} passes {g(7, np.max):7.2f} "
+                          f"{g(8, np.max):7.2f} {g(9, np.max):7.2f} {g(10, np.max):7.2f}")
+                continue
+            t = tr[l]
+            live = t[:, 0] > 0
+            if not live.any():
+                continue
+            t = t[live]
+            f = lambda k, fn: (fn(t[:, k][t[:, k] > 0]) - t0) / 1e3 if (t[:, k] > 0).any() else float("nan")
+            print(f"   L{l:2d}: {f(0, np.min):7.2f} {f(1, np.median):7.2f} {f(2, np.median):7.2f} "
+                  f"{f(3, np.median):7.2f} {f(3, np.max):7.2f} {f(5, np.median):7.2f} {f(7, np.median):7.2f} "
+                  f"{f(7, np.max):7.2f} {f(9, np.max):7.2f} {f(6, np.max):7.2f}")
 
 
 if __name__ == "__main__":
