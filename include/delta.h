@@ -73,9 +73,20 @@ typedef struct {
                                   P = page-level; page mode needs P | k (R6) */
     delta_dtype kv_dtype;      /* dtype of K/V pools, q, k_new, v_new.  Outputs are fp32. */
     float softmax_scale;       /* 0 -> (float)(1/sqrt(d))  (Eq.4, R16) */
-    int32_t shard_world;       /* sequence sharding across GPUs; 1 = off (must be 1 in this build) */
-    int32_t shard_rank;
-    const void* nccl_id;       /* reserved for sequence sharding */
+    int32_t shard_world;       /* W: sequence sharding across W GPUs (1 = off).  Rank r holds the
+                                  contiguous page range delta_shard_range() returns of EVERY
+                                  sequence (its kv_pool / block table need only those pages);
+                                  every layer all-gathers the per-rank (o, lse) partials and
+                                  LSE-merges them, every Delta layer also all-gathers its top-k
+                                  candidates.  All ranks make the same calls. */
+    int32_t shard_rank;        /* r in [0, W) */
+    const void* nccl_id;       /* W > 1: 128-byte ncclUniqueId (delta_nccl_get_unique_id on rank 0,
+                                  broadcast by the caller) -> the library owns an NCCL communicator
+                                  and runs both exchanges itself, on the call's stream (graph-
+                                  capturable).  NULL -> "external exchange": decode/select stop
+                                  after the local pass and the caller moves the bytes itself
+                                  (delta_shard_exchange_buffers) and calls delta_shard_merge /
+                                  delta_shard_select_merge (used for single-GPU simulation). */
 } delta_config;
 
 /* Caller-owned device buffers.  Sizes from delta_query_sizes. */
@@ -171,6 +182,32 @@ delta_status delta_decode_step_host(delta_t h, int32_t batch, const void* q_all_
 /* Synchronises `stream`, reads and clears the sticky device error flag.
  * *sticky = DELTA_OK or the first device-side error recorded. The only syncing call. */
 delta_status delta_get_error(delta_t h, cudaStream_t stream, delta_status* sticky);
+
+/* ---- sequence sharding (shard_world > 1) -------------------------------------------
+ * Rank 0 calls delta_nccl_get_unique_id; the 128 bytes are broadcast to all ranks (e.g. with
+ * torch.distributed) and passed as delta_config.nccl_id.  NCCL is loaded at run time
+ * (libnccl.so.2 already in the process, else $DELTA_NCCL_LIB).  DELTA_ERR_NCCL if absent. */
+delta_status delta_nccl_get_unique_id(void* out_128_bytes);
+
+/* Host-only: the page range [*page_lo, *page_hi) of every sequence that rank cfg->shard_rank
+ * holds (contiguous, page-aligned shares of ceil(max_seq_len/P) pages); [0, pages) if W = 1. */
+delta_status delta_shard_range(const delta_config* cfg, int32_t* page_lo, int32_t* page_hi);
+
+/* External-exchange mode (nccl_id == NULL).  which = 0: attention partials (after every
+ * delta_decode_layer / delta_append_decode_layer), 1: Delta-layer candidates (after
+ * delta_select).  The caller must make recv = the concatenation, in rank order, of every
+ * rank's send block (block_bytes each): an all-gather.  Device pointers into the workspace. */
+delta_status delta_shard_exchange_buffers(delta_t h, int32_t which, void** send, void** recv,
+                                          size_t* block_bytes);
+/* After the attention exchange: LSE-merge the ranks' partials in rank order -> out [batch][m][d],
+ * lse_out (optional) — identical on every rank.  PAPER.md:61-67 (any partition of the attended
+ * set gives the same softmax). */
+delta_status delta_shard_merge(delta_t h, int32_t layer, int32_t batch, float* out, float* lse_out,
+                               cudaStream_t stream);
+/* After the candidate exchange: global top-k over all ranks' candidates + the forced units ->
+ * the plan (and optional idx_out / count_out as in delta_select). */
+delta_status delta_shard_select_merge(delta_t h, int32_t layer, int32_t batch, int32_t* idx_out,
+                                      int32_t* count_out, cudaStream_t stream);
 
 delta_role   delta_layer_role(delta_t h, int32_t layer);        /* -1 cast if out of range */
 int32_t      delta_governing_layer(delta_t h, int32_t layer);  /* Delta layer of a SPARSE layer */

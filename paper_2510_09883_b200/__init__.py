@@ -4,7 +4,8 @@ The product is ``libdelta.so`` (C ABI in ``include/delta.h``; sm_100a kernels in
 ``csrc/``); :mod:`.binding` is a thin ctypes layer over it.
 """
 from .binding import (DELTA_BF16, DELTA_FP32, ROLE_FULL, ROLE_SELECT, ROLE_SPARSE, DeltaConfig, DeltaError,
-                      DeltaStack, declared_functions, load_library, query_sizes)
+                      DeltaStack, declared_functions, load_library, nccl_unique_id, query_sizes, shard_range)
 
 __all__ = ["DELTA_BF16", "DELTA_FP32", "ROLE_FULL", "ROLE_SELECT", "ROLE_SPARSE", "DeltaConfig", "DeltaError",
-           "DeltaStack", "declared_functions", "load_library", "query_sizes"]
+           "DeltaStack", "declared_functions", "load_library", "nccl_unique_id", "query_sizes",
+           "shard_range"]

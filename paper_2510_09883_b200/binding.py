@@ -93,6 +93,17 @@ def load_library() -> ctypes.CDLL:
     L.delta_destroy.restype = st
     L.delta_kernels_launched.argtypes = [vp]
     L.delta_kernels_launched.restype = ctypes.c_uint64
+    L.delta_nccl_get_unique_id.argtypes = [vp]
+    L.delta_nccl_get_unique_id.restype = st
+    L.delta_shard_range.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    L.delta_shard_range.restype = st
+    L.delta_shard_exchange_buffers.argtypes = [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                               ctypes.POINTER(ctypes.c_size_t)]
+    L.delta_shard_exchange_buffers.restype = st
+    L.delta_shard_merge.argtypes = [vp, i32, i32, vp, vp, vp]
+    L.delta_shard_merge.restype = st
+    L.delta_shard_select_merge.argtypes = [vp, i32, i32, vp, vp, vp]
+    L.delta_shard_select_merge.restype = st
     _lib = L
     return L
 
@@ -125,14 +136,17 @@ class DeltaConfig:
     num_phys_pages: int = 0
     shard_world: int = 1
     shard_rank: int = 0
+    nccl_id: bytes | None = None   # 128 bytes from nccl_unique_id() (rank 0), or None
 
     def to_c(self):
         arr = (ctypes.c_int32 * max(1, len(self.select_layers)))(*self.select_layers)
+        nid = ctypes.create_string_buffer(self.nccl_id, 128) if self.nccl_id else None
         c = _Config(self.num_layers, self.num_q_heads, self.num_kv_heads, self.head_dim, self.max_batch,
                     self.max_seq_len, self.page_size, self.num_phys_pages, self.num_full_prefix,
                     len(self.select_layers), arr, self.budget_k, self.n_sink, self.n_window, self.select_block,
-                    self.kv_dtype, self.softmax_scale, self.shard_world, self.shard_rank, None)
-        return c, arr  # keep arr alive
+                    self.kv_dtype, self.softmax_scale, self.shard_world, self.shard_rank,
+                    ctypes.cast(nid, ctypes.c_void_p) if nid is not None else None)
+        return c, (arr, nid)  # keep alive
 
     @property
     def max_pages(self) -> int:
@@ -155,6 +169,28 @@ def query_sizes(cfg: DeltaConfig) -> tuple[int, int]:
     pb, wb = ctypes.c_size_t(), ctypes.c_size_t()
     _check(L.delta_query_sizes(ctypes.byref(c), ctypes.byref(pb), ctypes.byref(wb)))
     return pb.value, wb.value
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId from rank 0 (to broadcast with torch.distributed)."""
+    import os
+    if "DELTA_NCCL_LIB" not in os.environ:
+        try:
+            import nvidia.nccl  # the copy torch uses
+            os.environ["DELTA_NCCL_LIB"] = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+        except Exception:  # noqa: BLE001
+            pass
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().delta_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+def shard_range(cfg: DeltaConfig) -> tuple[int, int]:
+    """[page_lo, page_hi) of every sequence held by rank cfg.shard_rank (host-only)."""
+    c, _keep = cfg.to_c()
+    lo, hi = ctypes.c_int32(), ctypes.c_int32()
+    _check(load_library().delta_shard_range(ctypes.byref(c), ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
 
 
 def _ptr(t) -> int | None:
@@ -235,6 +271,21 @@ class DeltaStack:
     def decode_step_host(self, q_host, k_host, v_host, out_host, stream=None):
         _check(self.lib.delta_decode_step_host(self.h, q_host.shape[1], q_host.data_ptr(), k_host.data_ptr(),
                                                v_host.data_ptr(), out_host.data_ptr(), _stream(stream)), self.h)
+
+    def exchange_buffers(self, which: int):
+        """(send_ptr, recv_ptr, block_bytes) of the external exchange (0: attention, 1: candidates)."""
+        s_, r_, n_ = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_size_t()
+        _check(self.lib.delta_shard_exchange_buffers(self.h, which, ctypes.byref(s_), ctypes.byref(r_),
+                                                     ctypes.byref(n_)), self.h)
+        return s_.value, r_.value, n_.value
+
+    def shard_merge(self, layer: int, out, lse=None, stream=None):
+        _check(self.lib.delta_shard_merge(self.h, layer, out.shape[0], out.data_ptr(), _ptr(lse), _stream(stream)),
+               self.h)
+
+    def shard_select_merge(self, layer: int, batch: int, idx_out=None, count_out=None, stream=None):
+        _check(self.lib.delta_shard_select_merge(self.h, layer, batch, _ptr(idx_out), _ptr(count_out),
+                                                 _stream(stream)), self.h)
 
     def get_error(self, stream=None) -> int:
         v = ctypes.c_int()

@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
         const int hh = (i / chunks) % p.g;
         const int tok = i / (chunks * p.g);
         const int t = n + tok;
+        if (t / kPage < p.page_lo || t / kPage >= p.page_hi) continue;  // another rank's page
         const size_t row = kv_row((size_t)p.layer * p.num_phys + bt[t / kPage], p.g, hh, t % kPage);
         const size_t src_off = ((size_t)tok * p.g + hh) * row_bytes + (size_t)c * 16;
         const size_t dst_off = row * row_bytes + (size_t)c * 16;

@@ -41,19 +41,7 @@ __global__ void __launch_bounds__(NW * 32) attn_simt_kernel(const AttnParams p) 
     const bool token_plan = (p.role == kRoleSparse) && p.sel_block == 1;
     bool stale = false;
     int n_items = 0, unit0 = 0, e_end = 0;
-    if (!cap_err) {
-        if (p.role != kRoleSparse) {
-            const int npages = (s + kPage - 1) / kPage;
-            unit0 = (int)((long long)split * npages / p.nsplit);
-            n_items = (int)((long long)(split + 1) * npages / p.nsplit) - unit0;
-        } else {
-            stale = p.plan_stamp[b] != s;
-            const int cnt = stale ? 0 : p.plan_count[b];
-            unit0 = (int)((long long)split * cnt / p.nsplit);
-            e_end = (int)((long long)(split + 1) * cnt / p.nsplit);
-            n_items = token_plan ? (e_end - unit0 + 15) / 16 : e_end - unit0;
-        }
-    }
+    if (!cap_err) split_geometry(p, b, split, s, token_plan, unit0, n_items, e_end, stale);
     const int32_t* bt = p.block_table + (size_t)b * p.bt_stride;
     const int32_t* plan = p.plan_idx + (size_t)b * p.plan_cap;
     const size_t layer_ph = (size_t)p.layer * p.num_phys;
@@ -61,7 +49,7 @@ __global__ void __launch_bounds__(NW * 32) attn_simt_kernel(const AttnParams p) 
     const T* k_new = reinterpret_cast<const T*>(p.k_new) + ((size_t)b * p.g + h) * D;
     const T* v_new = reinterpret_cast<const T*>(p.v_new) + ((size_t)b * p.g + h) * D;
 
-    if (p.fuse_append && !cap_err && split == 0 && warp == 0) {  // Eq.7 append of head h
+    if (p.fuse_append && !cap_err && split == 0 && warp == 0 && owns_page(p, (s - 1) / kPage)) {  // Eq.7 append of head h
         const int t = s - 1;
         const size_t row = kv_row(layer_ph + bt[t / kPage], p.g, h, t % kPage);
         T* kd = reinterpret_cast<T*>(p.kv_pool) + row * D;

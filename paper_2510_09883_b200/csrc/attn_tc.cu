@@ -115,19 +115,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     const bool cap_err = s > p.max_seq;
     bool stale = false;
     int n_items = 0, unit0 = 0, e_end = 0;
-    if (!cap_err) {
-        if (p.role != kRoleSparse) {
-            const int npages = (s + kPage - 1) / kPage;
-            unit0 = (int)((long long)split * npages / p.nsplit);
-            n_items = (int)((long long)(split + 1) * npages / p.nsplit) - unit0;
-        } else {
-            stale = p.plan_stamp[b] != s;
-            const int cnt = stale ? 0 : p.plan_count[b];
-            unit0 = (int)((long long)split * cnt / p.nsplit);
-            e_end = (int)((long long)(split + 1) * cnt / p.nsplit);
-            n_items = TOKEN_PLAN ? (e_end - unit0 + 15) / 16 : e_end - unit0;
-        }
-    }
+    if (!cap_err) split_geometry(p, b, split, s, TOKEN_PLAN, unit0, n_items, e_end, stale);
     const int32_t* bt = p.block_table + (size_t)b * p.bt_stride;
     const int32_t* plan = p.plan_idx + (size_t)b * p.plan_cap;
     const int32_t* plan_phys = p.plan_phys + (size_t)b * p.plan_cap;
@@ -141,7 +129,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     const __nv_bfloat16* v_new = reinterpret_cast<const __nv_bfloat16*>(p.v_new) + ((size_t)b * p.g + h) * D;
 
     // fused append: split 0 writes the new row of head h to the pool (Eq.7)
-    if (p.fuse_append && !cap_err && split == 0 && warp == 0) {
+    if (p.fuse_append && !cap_err && split == 0 && warp == 0 && owns_page(p, (s - 1) / kPage)) {
         constexpr int kChunks = D / 8;
         const int t = s - 1;
         const size_t krow = kv_row(layer_ph + bt[t / kPage], p.g, h, t % kPage);

@@ -36,6 +36,32 @@ __device__ __forceinline__ void set_err(int32_t* err, int code) {
     if (err) atomicCAS(err, 0, code);
 }
 
+// Does this rank hold logical page u (sequence sharding; always true when unsharded)?
+__device__ __forceinline__ bool owns_page(const AttnParams& p, int u) { return u >= p.page_lo && u < p.page_hi; }
+
+// The units this CTA (split `split` of the nsplit CTAs of one (sequence, kv head)) attends:
+//  FULL / SELECT: pages [unit0, unit0 + n_items) of this rank's share of [0, ceil(s/P));
+//  SPARSE: plan entries [unit0, e_end) of this rank's share of the plan (n_items tiles of
+//  16 entries for a token plan); a stale plan (stamp != s) attends nothing (NaN outputs).
+__device__ __forceinline__ void split_geometry(const AttnParams& p, int b, int split, int s, bool token_plan,
+                                               int& unit0, int& n_items, int& e_end, bool& stale) {
+    if (p.role != kRoleSparse) {
+        const int npages = (s + kPage - 1) / kPage;
+        const int lo = max(0, p.page_lo), hi = min(npages, p.page_hi), n = max(0, hi - lo);
+        unit0 = lo + (int)((long long)split * n / p.nsplit);
+        n_items = lo + (int)((long long)(split + 1) * n / p.nsplit) - unit0;
+    } else {
+        stale = p.plan_stamp[b] != s;
+        const int cnt = stale ? 0 : p.plan_count[b];
+        const int elo = (p.plan_lo && !stale) ? p.plan_lo[b] : 0;
+        const int ehi = (p.plan_hi && !stale) ? p.plan_hi[b] : cnt;
+        const int n = max(0, ehi - elo);
+        unit0 = elo + (int)((long long)split * n / p.nsplit);
+        e_end = elo + (int)((long long)(split + 1) * n / p.nsplit);
+        n_items = token_plan ? (e_end - unit0 + 15) / 16 : e_end - unit0;
+    }
+}
+
 // Cluster split-K epilogue, called by EVERY thread of every CTA of the cluster (the
 // cluster = the `nsplit` CTAs of one (sequence, kv head); rank = split).  Push model, one
 // cluster barrier:
@@ -143,11 +169,16 @@ __device__ __forceinline__ void cluster_epilogue(const AttnParams& p, const floa
                 bad = true;
             }
             const int j = h * gs + row;
-            reinterpret_cast<float4*>(p.out + ((size_t)b * p.m + j) * D)[c4] = o;
+            const bool shard = p.shard_world > 1;  // the rank's partial; shard.cu merges the ranks
+            reinterpret_cast<float4*>((shard ? p.part_o : p.out) + ((size_t)b * p.m + j) * D)[c4] = o;
             if (c4 == 0) {
                 const float lse = (L > 0.f) ? (M + log2f(L)) * kLn2 : -INFINITY;
-                if (p.lse_out) p.lse_out[(size_t)b * p.m + j] = lse;
-                if (p.role == kRoleSelect) p.lse_buf[(size_t)b * p.m + j] = lse;
+                if (shard) {
+                    p.part_lse[(size_t)b * p.m + j] = lse;
+                } else {
+                    if (p.lse_out) p.lse_out[(size_t)b * p.m + j] = lse;
+                    if (p.role == kRoleSelect) p.lse_buf[(size_t)b * p.m + j] = lse;
+                }
             }
         }
     }

@@ -4,6 +4,8 @@
 // step driver.  All device work is in the kernels; this file only marshals and launches.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -26,8 +28,9 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
-    size_t seq_len, err, cnt_sel, logits, lse_buf, keys, plan_idx, plan_phys, plan_count, plan_stamp, stage_q, stage_k,
-        stage_v, stage_out, total;
+    size_t seq_len, err, cnt_sel, logits, lse_buf, keys, plan_idx, plan_phys, plan_count, plan_stamp, plan_lo, plan_hi,
+        shard_send, shard_recv, cand_send, cand_recv, stage_q, stage_k, stage_v, stage_out, total;
+    size_t shard_block, cand_block;  // bytes of one rank's attention partial / candidate block
     int max_units, plan_cap, n_delta, max_pages;
 };
 
@@ -83,7 +86,8 @@ std::string validate(const delta_config& c, std::vector<int>& role, std::vector<
     if (c.select_block != 1 && c.select_block != c.page_size) return "select_block must be 1 or page_size";
     if (c.select_block == c.page_size && c.budget_k % c.page_size != 0)
         return "page-level selection needs budget_k % page_size == 0 (R6)";
-    if (c.shard_world != 1 || c.shard_rank != 0) return "sequence sharding (shard_world > 1) is not built in this library version";
+    if (c.shard_world < 1 || c.shard_world > 64 || c.shard_rank < 0 || c.shard_rank >= c.shard_world)
+        return "shard_world must be in [1, 64] and 0 <= shard_rank < shard_world";
     if (c.softmax_scale < 0.f || !std::isfinite(c.softmax_scale)) return "softmax_scale must be finite and >= 0";
     role.assign(c.num_layers, kRoleSparse);
     gov.assign(c.num_layers, -1);
@@ -140,6 +144,17 @@ Layout layout(const delta_config& c, int sms) {
     L.plan_phys = take((size_t)nd * c.max_batch * L.plan_cap * 4);
     L.plan_count = take((size_t)nd * c.max_batch * 4);
     L.plan_stamp = take((size_t)nd * c.max_batch * 4);
+    L.plan_lo = take((size_t)nd * c.max_batch * 4);
+    L.plan_hi = take((size_t)nd * c.max_batch * 4);
+    {   // sequence sharding exchange buffers: partial (o [B][m][d], lse [B][m]) and candidates
+        const int W = std::max(1, c.shard_world);
+        L.shard_block = W > 1 ? align_up((size_t)c.max_batch * m * (D + 1) * 4) : 0;
+        L.cand_block = W > 1 && has_sel ? align_up((size_t)c.max_batch * L.plan_cap * 8) : 0;
+        L.shard_send = take(L.shard_block);
+        L.shard_recv = take(L.shard_block * W);
+        L.cand_send = take(L.cand_block);
+        L.cand_recv = take(L.cand_block * W);
+    }
     L.stage_q = take((size_t)c.num_layers * c.max_batch * m * D * e);
     L.stage_k = take((size_t)c.num_layers * c.max_batch * g * D * e);
     L.stage_v = take((size_t)c.num_layers * c.max_batch * g * D * e);
@@ -153,6 +168,52 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 }  // namespace
+
+// NCCL, loaded at run time (the library has no link-time NCCL dependency; in a torch process
+// dlopen finds the libnccl.so.2 torch already loaded, else DELTA_NCCL_LIB names it).
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) {
+            const char* env = std::getenv("DELTA_NCCL_LIB");
+            if (env) lib = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+        }
+        if (!lib) {
+            a.why = "libnccl.so.2 not found (set DELTA_NCCL_LIB)";
+            return a;
+        }
+        a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(lib, "ncclGetUniqueId"));
+        a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(dlsym(lib, "ncclCommInitRank"));
+        a.allGather = reinterpret_cast<decltype(a.allGather)>(dlsym(lib, "ncclAllGather"));
+        a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(lib, "ncclCommDestroy"));
+        a.getErrorString = reinterpret_cast<decltype(a.getErrorString)>(dlsym(lib, "ncclGetErrorString"));
+        a.ok = a.getUniqueId && a.commInitRank && a.allGather && a.commDestroy && a.getErrorString;
+        if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
+        return a;
+    }();
+    return api;
+}
+
+// Static page range of a rank: contiguous, page-aligned shares of the max_seq_len pages.
+void shard_pages(const delta_config& c, int rank, int* lo, int* hi) {
+    const int max_pages = (c.max_seq_len + kPage - 1) / kPage;
+    const int W = std::max(1, c.shard_world);
+    const int per = (max_pages + W - 1) / W;
+    *lo = std::min(max_pages, rank * per);
+    *hi = std::min(max_pages, (rank + 1) * per);
+    if (W == 1) { *lo = 0; *hi = 0x7fffffff; }
+}
 
 namespace delta {
 int cluster_limit(const void* kern, int threads, int smem_bytes) {
@@ -198,6 +259,9 @@ struct delta_ctx {
     bool pdl = true;
     int tune_nsplit = 0, tune_deep = -1;  // DELTA_TUNE overrides (0 / -1 = automatic)
     int tune_prewait = 1, tune_early = 1;
+    // sequence sharding
+    int world = 1, rank = 0, page_lo = 0, page_hi = 0x7fffffff;
+    ncclComm_t comm = nullptr;  // null with world > 1: the caller exchanges (delta_shard_* calls)
     // the previous kernel this handle enqueued (decides whether the next attention kernel
     // may start its KV stream before griddepcontrol.wait; see attn_tc.cu)
     enum { kLastNone, kLastAttn, kLastSelect, kLastAppend } last_kind = kLastNone;
@@ -242,6 +306,18 @@ AttnParams attn_params(delta_ctx* h, int layer, int batch) {
     } else {
         p.nsplit = nsplit_full(batch, c.num_kv_heads, h->sms, h->L.max_pages);
     }
+    p.shard_world = h->world;
+    p.page_lo = h->page_lo;
+    p.page_hi = h->page_hi;
+    if (h->world > 1) {
+        p.part_o = h->at<float>(h->L.shard_send);
+        p.part_lse = p.part_o + (size_t)batch * c.num_q_heads * c.head_dim;
+        if (p.role == kRoleSparse) {
+            const int sl = h->slot[h->gov[layer]];
+            p.plan_lo = h->at<int32_t>(h->L.plan_lo) + (size_t)sl * c.max_batch;
+            p.plan_hi = h->at<int32_t>(h->L.plan_hi) + (size_t)sl * c.max_batch;
+        }
+    }
     if (h->tune_nsplit > 0) p.nsplit = std::min(h->tune_nsplit, kMaxSplit);
     p.deep = deep_ring(batch, c.num_kv_heads, p.nsplit, h->sms) ? 1 : 0;
     if (h->tune_deep >= 0) p.deep = h->tune_deep;
@@ -265,6 +341,31 @@ delta_status check_sparse_fresh(delta_ctx* h, int layer, bool appending) {
         return fail(h, DELTA_ERR_USAGE,
                     "stale plan: layer " + std::to_string(layer) + " needs delta_select on Delta layer " +
                         std::to_string(d) + " at this step (PAPER.md:160-161)");
+    return DELTA_OK;
+}
+
+delta_status shard_allgather(delta_ctx* h, size_t send_off, size_t recv_off, size_t bytes, cudaStream_t st) {
+    ncclResult_t r = nccl().allGather(h->ws + send_off, h->ws + recv_off, bytes, ncclUint8, h->comm, st);
+    if (r != ncclSuccess) return fail(h, DELTA_ERR_NCCL, std::string("ncclAllGather: ") + nccl().getErrorString(r));
+    return DELTA_OK;
+}
+
+// Cross-rank LSE merge of the attention partials (shard.cu) -> out, lse_out (and the Delta
+// layer's global LSE for scoring).
+delta_status launch_merge(delta_ctx* h, int layer, int batch, float* out, float* lse_out, cudaStream_t st) {
+    const delta_config& c = h->cfg;
+    ShardMergeParams mp = {};
+    mp.world = h->world; mp.batch = batch; mp.m = c.num_q_heads; mp.d = c.head_dim; mp.role = h->role[layer];
+    mp.recv_o = h->at<float>(h->L.shard_recv);
+    mp.recv_lse = mp.recv_o + (size_t)batch * c.num_q_heads * c.head_dim;
+    mp.o_stride = mp.lse_stride = h->L.shard_block / 4;
+    mp.out = out; mp.lse_out = lse_out; mp.lse_buf = h->at<float>(h->L.lse_buf);
+    mp.err = h->at<int32_t>(h->L.err);
+    cudaError_t e = launch_shard_merge(mp, st, h->pdl);
+    if (e != cudaSuccess) return cuda_fail(h, e, "shard merge launch");
+    ++h->launches;
+    h->last_kind = delta_ctx::kLastAttn;
+    h->last_layer = layer;
     return DELTA_OK;
 }
 
@@ -292,11 +393,16 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
     ++h->launches;
     h->last_kind = delta_ctx::kLastAttn;
     h->last_layer = layer;
+    if (h->world > 1 && h->comm) {  // sequence sharding: all-gather the partials, then merge
+        delta_status s2 = shard_allgather(h, h->L.shard_send, h->L.shard_recv, h->L.shard_block, st);
+        if (s2 != DELTA_OK) return s2;
+        return launch_merge(h, layer, batch, out, lse_out, st);
+    }
     return DELTA_OK;
 }
 
 delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_override, int32_t* idx_out,
-                        int32_t* count_out, cudaStream_t st) {
+                        int32_t* count_out, cudaStream_t st, int shard_mode = 0) {
     const delta_config& c = h->cfg;
     SelectParams p = {};
     const int sl = h->slot[layer];
@@ -315,6 +421,11 @@ delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_ov
     p.plan_stamp = h->at<int32_t>(h->L.plan_stamp) + (size_t)sl * c.max_batch;
     p.idx_out = idx_out; p.count_out = count_out;
     p.cnt = h->at<int32_t>(h->L.cnt_sel) + (size_t)layer * c.max_batch;
+    p.shard_mode = shard_mode;
+    p.page_lo = h->page_lo; p.page_hi = h->page_hi;
+    p.cand_out = h->at<uint2>(h->L.cand_send);
+    p.plan_lo = h->at<int32_t>(h->L.plan_lo) + (size_t)sl * c.max_batch;
+    p.plan_hi = h->at<int32_t>(h->L.plan_hi) + (size_t)sl * c.max_batch;
     p.err = h->at<int32_t>(h->L.err);
     cudaError_t e = launch_select(p, st, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "select launch");
@@ -322,6 +433,31 @@ delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_ov
     h->last_kind = delta_ctx::kLastSelect;
     h->last_layer = layer;
     return DELTA_OK;
+}
+
+// Global selection merge (sequence sharding): dense keys from every rank's candidates, then
+// the unchanged forced-union + top-k (select.cu shard_mode 2).
+delta_status launch_sel_merge(delta_ctx* h, int layer, int batch, int32_t* idx_out, int32_t* count_out,
+                              cudaStream_t st) {
+    const delta_config& c = h->cfg;
+    float* keys = h->at<float>(h->L.keys);
+    cudaError_t e = launch_cand_scatter(h->at<uint2>(h->L.cand_recv), h->world, batch, h->L.plan_cap,
+                                        h->L.cand_block / 8, keys, h->L.max_units, h->at<int32_t>(h->L.seq_len),
+                                        layer, c.max_batch, c.num_kv_heads, c.select_block, st, h->pdl);
+    if (e != cudaSuccess) return cuda_fail(h, e, "candidate scatter launch");
+    ++h->launches;
+    return launch_sel(h, layer, batch, keys, idx_out, count_out, st, 2);
+}
+
+// Sharded selection: local candidates, exchange, merge (or stop after the local pass when the
+// caller runs the exchange itself).
+delta_status launch_sel_sharded(delta_ctx* h, int layer, int batch, int32_t* idx_out, int32_t* count_out,
+                                cudaStream_t st) {
+    delta_status s = launch_sel(h, layer, batch, nullptr, nullptr, nullptr, st, 1);
+    if (s != DELTA_OK || !h->comm) return s;
+    s = shard_allgather(h, h->L.cand_send, h->L.cand_recv, h->L.cand_block, st);
+    if (s != DELTA_OK) return s;
+    return launch_sel_merge(h, layer, batch, idx_out, count_out, st);
 }
 
 // enqueue one whole step (fused append + decode per layer, select after Delta layers)
@@ -340,7 +476,8 @@ delta_status enqueue_step(delta_ctx* h, int batch, const void* q_all, const void
                                        lse_all ? lse_all + (size_t)l * batch * c.num_q_heads : nullptr, st, true);
         if (s != DELTA_OK) return s;
         if (h->role[l] == kRoleSelect) {
-            s = launch_sel(h, l, batch, nullptr, nullptr, nullptr, st);
+            s = h->world > 1 ? launch_sel_sharded(h, l, batch, nullptr, nullptr, st)
+                             : launch_sel(h, l, batch, nullptr, nullptr, nullptr, st);
             if (s != DELTA_OK) return s;
         }
     }
@@ -449,6 +586,25 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
         delete h;
         return fail(nullptr, DELTA_ERR_CUDA, m);
     }
+    h->world = std::max(1, cfg->shard_world);
+    h->rank = cfg->shard_rank;
+    shard_pages(h->cfg, h->rank, &h->page_lo, &h->page_hi);
+    if (h->world > 1 && cfg->nccl_id) {
+        const NcclApi& api = nccl();
+        if (!api.ok) {
+            std::string m = api.why;
+            delete h;
+            return fail(nullptr, DELTA_ERR_NCCL, m);
+        }
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_id, sizeof id);
+        ncclResult_t r = api.commInitRank(&h->comm, h->world, id, h->rank);
+        if (r != ncclSuccess) {
+            std::string m = std::string("ncclCommInitRank: ") + api.getErrorString(r);
+            delete h;
+            return fail(nullptr, DELTA_ERR_NCCL, m);
+        }
+    }
     // Tuning hook for kernel experiments (tools/trace_probe.py): DELTA_TUNE="nsplit=N,deep=0|1".
     if (const char* t = std::getenv("DELTA_TUNE")) {
         const char* a = std::strstr(t, "nsplit=");
@@ -468,6 +624,7 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
 delta_status delta_destroy(delta_t h) {
     if (!h) return DELTA_ERR_USAGE;
     if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    if (h->comm) nccl().commDestroy(h->comm);
     delete h;
     return DELTA_OK;
 }
@@ -508,6 +665,7 @@ delta_status delta_append_kv(delta_t h, int32_t layer, int32_t batch, int32_t nt
     p.max_seq = h->cfg.max_seq_len; p.elem_bytes = elem_bytes(h->cfg);
     p.k_new = k_new; p.v_new = v_new; p.kv_pool = h->kv_pool;
     p.block_table = h->block_table; p.seq_len = h->at<int32_t>(h->L.seq_len); p.err = h->at<int32_t>(h->L.err);
+    p.page_lo = h->page_lo; p.page_hi = h->page_hi;
     cudaError_t e = launch_append(p, stream, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "append launch");
     ++h->launches;
@@ -552,7 +710,11 @@ delta_status delta_select(delta_t h, int32_t layer, int32_t batch, const float* 
     if (h->role[layer] != kRoleSelect) return fail(h, DELTA_ERR_USAGE, "delta_select on a non-Delta layer");
     if (!keys_override && h->dec_step[layer] != h->step[layer])
         return fail(h, DELTA_ERR_USAGE, "delta_select needs this layer's decode at the current step");
-    s = launch_sel(h, layer, batch, keys_override, idx_out, count_out, stream);
+    if (h->world > 1)  // sharded: local candidates + exchange + global merge (a key override is global)
+        s = keys_override ? launch_sel(h, layer, batch, keys_override, idx_out, count_out, stream, 2)
+                          : launch_sel_sharded(h, layer, batch, idx_out, count_out, stream);
+    else
+        s = launch_sel(h, layer, batch, keys_override, idx_out, count_out, stream);
     if (s == DELTA_OK) h->sel_step[h->slot[layer]] = h->step[layer];
     return s;
 }
@@ -560,6 +722,8 @@ delta_status delta_select(delta_t h, int32_t layer, int32_t batch, const float* 
 delta_status delta_decode_step(delta_t h, int32_t batch, const void* q_all, const void* k_all, const void* v_all,
                                float* out_all, float* lse_all, cudaStream_t stream) {
     if (!h) return fail(nullptr, DELTA_ERR_USAGE, "null handle");
+    if (h->world > 1 && !h->comm)
+        return fail(h, DELTA_ERR_USAGE, "sharded handle without NCCL: drive layers with the delta_shard_* calls");
     if (batch < 1 || batch > h->cfg.max_batch) return fail(h, DELTA_ERR_USAGE, "batch out of range");
     if (!q_all || !k_all || !v_all || !out_all) return fail(h, DELTA_ERR_USAGE, "null pointer");
     const bool legacy = (stream == 0 || stream == cudaStreamLegacy || stream == cudaStreamPerThread);
@@ -654,5 +818,57 @@ int32_t delta_plan_capacity(delta_t h) { return h ? h->L.plan_cap : -1; }
 const char* delta_last_error_message(delta_t h) { return h ? h->msg.c_str() : g_msg.c_str(); }
 
 uint64_t delta_kernels_launched(delta_t h) { return h ? h->launches : 0; }
+
+delta_status delta_nccl_get_unique_id(void* out_128_bytes) {
+    if (!out_128_bytes) return fail(nullptr, DELTA_ERR_USAGE, "null argument");
+    const NcclApi& api = nccl();
+    if (!api.ok) return fail(nullptr, DELTA_ERR_NCCL, api.why);
+    ncclUniqueId id;
+    ncclResult_t r = api.getUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, DELTA_ERR_NCCL, std::string("ncclGetUniqueId: ") + api.getErrorString(r));
+    std::memcpy(out_128_bytes, &id, sizeof id);
+    return DELTA_OK;
+}
+
+delta_status delta_shard_range(const delta_config* cfg, int32_t* page_lo, int32_t* page_hi) {
+    if (!cfg || !page_lo || !page_hi) return fail(nullptr, DELTA_ERR_USAGE, "null argument");
+    std::vector<int> role, gov;
+    std::string err = validate(*cfg, role, gov);
+    if (!err.empty()) return fail(nullptr, DELTA_ERR_CONFIG, err);
+    int lo, hi;
+    shard_pages(*cfg, cfg->shard_rank, &lo, &hi);
+    const int max_pages = (cfg->max_seq_len + kPage - 1) / kPage;
+    *page_lo = cfg->shard_world > 1 ? lo : 0;
+    *page_hi = cfg->shard_world > 1 ? hi : max_pages;
+    return DELTA_OK;
+}
+
+delta_status delta_shard_exchange_buffers(delta_t h, int32_t which, void** send, void** recv, size_t* block_bytes) {
+    if (!h || !send || !recv || !block_bytes) return fail(h, DELTA_ERR_USAGE, "null argument");
+    if (h->world < 2) return fail(h, DELTA_ERR_USAGE, "not a sharded handle");
+    if (which != 0 && which != 1) return fail(h, DELTA_ERR_USAGE, "which must be 0 (attention) or 1 (candidates)");
+    *send = h->ws + (which == 0 ? h->L.shard_send : h->L.cand_send);
+    *recv = h->ws + (which == 0 ? h->L.shard_recv : h->L.cand_recv);
+    *block_bytes = which == 0 ? h->L.shard_block : h->L.cand_block;
+    return DELTA_OK;
+}
+
+delta_status delta_shard_merge(delta_t h, int32_t layer, int32_t batch, float* out, float* lse_out,
+                               cudaStream_t stream) {
+    delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    if (h->world < 2 || h->comm) return fail(h, DELTA_ERR_USAGE, "delta_shard_merge needs a sharded handle without NCCL");
+    if (!out) return fail(h, DELTA_ERR_USAGE, "null out");
+    return launch_merge(h, layer, batch, out, lse_out, stream);
+}
+
+delta_status delta_shard_select_merge(delta_t h, int32_t layer, int32_t batch, int32_t* idx_out,
+                                      int32_t* count_out, cudaStream_t stream) {
+    delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    if (h->world < 2 || h->comm) return fail(h, DELTA_ERR_USAGE, "delta_shard_select_merge needs a sharded handle without NCCL");
+    if (h->role[layer] != kRoleSelect) return fail(h, DELTA_ERR_USAGE, "not a Delta layer");
+    return launch_sel_merge(h, layer, batch, idx_out, count_out, stream);
+}
 
 }  // extern "C"

@@ -52,6 +52,14 @@ struct AttnParams {
     const int32_t* plan_count;  // [max_batch]
     const int32_t* plan_stamp;  // [max_batch]
     int32_t* err;
+    // sequence sharding (shard_world > 1): this rank holds pages [page_lo, page_hi) of every
+    // sequence; attention covers only those, and the epilogue writes the rank's partial
+    // (normalised o, natural-log lse) instead of the outputs, for the cross-rank LSE merge.
+    int shard_world, page_lo, page_hi;
+    const int32_t* plan_lo;     // SPARSE, sharded: [max_batch] this rank's plan entries [lo, hi)
+    const int32_t* plan_hi;
+    float* part_o;              // [batch][m][d]
+    float* part_lse;            // [batch][m]
 };
 
 // Score + top-k selection launch (one Delta layer).
@@ -74,10 +82,31 @@ struct SelectParams {
     int32_t* count_out;         // optional [batch]
     int32_t* cnt;               // [max_batch] arrival counters (this layer)
     int32_t* err;
+    // sequence sharding: mode 0 = unsharded; 1 = local (keys of own units only; export the
+    // rank's top-k candidates to cand_out); 2 = global merge (keys_override = the dense keys
+    // scattered from all ranks' candidates; also writes this rank's plan range lo/hi)
+    int shard_mode, page_lo, page_hi;
+    uint2* cand_out;            // mode 1: [batch][k_units] (order-preserving key bits, unit)
+    int32_t* plan_lo;           // [max_batch]
+    int32_t* plan_hi;
+};
+
+// Cross-rank merge of attention partials (sequence sharding): recv [W][batch][m][d] o and
+// [W][batch][m] lse (natural), fixed rank order.
+struct ShardMergeParams {
+    int world, batch, m, d, role;
+    const float* recv_o;        // [W][batch][m][d]
+    const float* recv_lse;      // [W][batch][m]
+    size_t o_stride, lse_stride;  // floats between ranks
+    float* out;                 // [batch][m][d]
+    float* lse_out;             // [batch][m] or null
+    float* lse_buf;             // SELECT: [max_batch][m]
+    int32_t* err;
 };
 
 struct AppendParams {
     int g, d, layer, batch, ntok, num_phys, bt_stride, max_batch, max_seq, elem_bytes;
+    int page_lo, page_hi;  // sequence sharding: this rank writes rows on its pages only
     const void* k_new;  // [batch][ntok][g][d]
     const void* v_new;
     void* kv_pool;
@@ -93,6 +122,11 @@ cudaError_t launch_attn_simt(const AttnParams& p, bool bf16, cudaStream_t st, bo
 cudaError_t launch_select(const SelectParams& p, cudaStream_t st, bool pdl);
 cudaError_t launch_append(const AppendParams& p, cudaStream_t st, bool pdl);
 size_t select_smem_bytes(int max_units);
+cudaError_t launch_shard_merge(const ShardMergeParams& p, cudaStream_t st, bool pdl);
+// scatter W x k candidates (uint2 key bits / unit) into dense fp32 keys (-inf elsewhere)
+cudaError_t launch_cand_scatter(const uint2* recv, int world, int batch, int k_units, size_t rank_stride,
+                                float* keys, int max_units, const int32_t* seq_len, int layer, int max_batch,
+                                int g, int sel_block, cudaStream_t st, bool pdl);
 // Largest cluster size (16, 8, 4, 2 or 1) with which `kern` can be resident (delta_api.cu).
 int cluster_limit(const void* kern, int threads, int smem_bytes);
 

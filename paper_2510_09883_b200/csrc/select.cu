@@ -135,24 +135,30 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
         const float* lg = p.logits + (size_t)b * p.max_seq * p.m;
         const int jr = lane >> 1, hh = lane & 1;
         // a warp handles 16 consecutive tokens: lane = 2*token + half-of-heads
+        // sequence-sharded local pass: only this rank's pages carry logits; the other units'
+        // keys are -inf (never a candidate of this rank)
+        const int own_lo = p.shard_mode == 1 ? p.page_lo * kPage : 0;
+        const int own_hi = p.shard_mode == 1 ? p.page_hi * kPage : 0x7fffffff;
         if (block == kPage) {
             for (int u = u_lo + warp; u < u_hi; u += kSelWarps) {
                 const int t = u * kPage + jr;
+                const bool own = t >= own_lo && t < own_hi;
                 float mx = -INFINITY;
-                if (t < s) mx = head_max(lg + (size_t)t * p.m, lsl, lse_g, p.m, hh);
+                if (t < s && own) mx = head_max(lg + (size_t)t * p.m, lsl, lse_g, p.m, hh);
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
                 const float e = (t < s) ? expf(mx) : 0.f;
                 float sum = 0.f;
 #pragma unroll
                 for (int r = 0; r < kPage; ++r) sum += __shfl_sync(0xffffffffu, e, 2 * r);  // ascending t
-                if (lane == 0) keys_b[u] = sum;
+                if (lane == 0) keys_b[u] = (u * kPage >= own_lo && u * kPage < own_hi) ? sum : -INFINITY;
             }
         } else {
             const int t_lo = u_lo, t_hi = u_hi;  // block == 1: units are tokens
             for (int t0 = t_lo + warp * 16; t0 < t_hi; t0 += kSelWarps * 16) {
                 const int t = t0 + jr;
+                const bool own = t >= own_lo && t < own_hi;
                 float mx = -INFINITY;
-                if (t < t_hi) mx = head_max(lg + (size_t)t * p.m, lsl, lse_g, p.m, hh);
+                if (t < t_hi && own) mx = head_max(lg + (size_t)t * p.m, lsl, lse_g, p.m, hh);
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
                 if (t < t_hi && hh == 0) keys_b[t] = mx;
             }
@@ -322,10 +328,43 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
     }
     __syncthreads();
     if (tid == 0) DTRACE(5);
+    const int n_plan = min(count, p.plan_cap);
+    if (p.shard_mode == 1) {
+        // export this rank's candidates: its non-forced plan units with a real key
+        uint2* cand = p.cand_out + (size_t)b * p.plan_cap;
+        for (int i = tid; i < p.plan_cap; i += kSelThreads) {
+            uint2 c = make_uint2(0u, 0xffffffffu);  // (key bits, unit = -1): empty slot
+            if (i < n_plan) {
+                const int u = plan[i];
+                const float key = __ldcg(src + u);
+                if (!forced(u) && key != -INFINITY) c = make_uint2(__float_as_uint(key), (uint32_t)u);
+            }
+            cand[i] = c;
+        }
+        return;  // the global plan comes from the merge pass (shard_mode 2)
+    }
+    if (p.shard_mode == 2 && tid < 32) {
+        // this rank's sub-range of the ascending global plan: units on its pages
+        int below_lo = 0, below_hi = 0;
+        for (int i = lane; i < n_plan; i += 32) {
+            const int pg = block == 1 ? plan[i] / kPage : plan[i];
+            below_lo += pg < p.page_lo;
+            below_hi += pg < p.page_hi;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            below_lo += __shfl_xor_sync(0xffffffffu, below_lo, off);
+            below_hi += __shfl_xor_sync(0xffffffffu, below_hi, off);
+        }
+        if (lane == 0) {
+            p.plan_lo[b] = below_lo;
+            p.plan_hi[b] = below_hi;
+        }
+    }
     if (tid == 0) {
-        p.plan_count[b] = min(count, p.plan_cap);
+        p.plan_count[b] = n_plan;
         p.plan_stamp[b] = s;
-        if (p.count_out) p.count_out[b] = min(count, p.plan_cap);
+        if (p.count_out) p.count_out[b] = n_plan;
     }
     if (p.idx_out) {
         __syncthreads();

@@ -68,7 +68,8 @@ def test_tier_validation_matches_paper(ex):
     dict(num_q_heads=64, num_kv_heads=2),       # gs <= 16
     dict(select_layers=[16, 2, 25]),            # ascending
     dict(num_full_prefix=3),                    # Delta layer 2 inside the full prefix
-    dict(shard_world=2),                        # not built
+    dict(shard_world=2, shard_rank=2),          # rank outside [0, W)
+    dict(shard_world=0),                        # W >= 1
 ])
 def test_config_errors(bad):
     with pytest.raises(DeltaError, match="CONFIG"):
@@ -81,3 +82,14 @@ def test_null_handle_calls_are_usage_errors():
     assert lib.delta_select(None, 0, 1, None, None, None, None) == 2
     assert lib.delta_layer_role(None, 0) == -1
     assert lib.delta_destroy(None) == 2
+
+
+def test_shard_ranges_partition_the_pages():
+    """Host-only: the ranks' page ranges are contiguous, disjoint and cover ceil(max_seq/P)."""
+    for W in (1, 2, 3, 4, 8):
+        for max_seq in (16, 1000, 32768 + 64, 131072 + 64):
+            pages = -(-max_seq // 16)
+            got = [d200.shard_range(_c1(max_seq_len=max_seq, shard_world=W, shard_rank=r)) for r in range(W)]
+            assert got[0][0] == 0 and got[-1][1] == pages
+            for (lo, hi), (lo2, _) in zip(got, got[1:]):
+                assert lo <= hi == lo2
