@@ -41,8 +41,10 @@ CONFIGS = {
                L=32, m=32, g=8, d=128, batch=1, ctx=32768, k=2048, delta=[2, 16, 25], F=2, scaling="weak"),
     "c2": dict(workload="DeepSeek-R1-Distill-Qwen-7B shape (28L, 28q/4kv, d128, bf16) b=32 ctx 16K budget 4K",
                L=28, m=28, g=4, d=128, batch=32, ctx=16384, k=4096, delta=[2, 14, 22], F=2, scaling="strong"),
-    "c3": dict(workload="Llama-8B shape b=1 ctx 128K budget 2K (single GPU; sequence sharding not built)",
-               L=32, m=32, g=8, d=128, batch=1, ctx=131072, k=2048, delta=[2, 16, 25], F=2, scaling="weak"),
+    "c3": dict(workload="Llama-8B shape b=1 ctx 128K budget 2K, KV sequence-sharded over the GPUs (NCCL LSE "
+                        "partial merge + global top-k candidate merge)",
+               L=32, m=32, g=8, d=128, batch=1, ctx=131072, k=2048, delta=[2, 16, 25], F=2, scaling="strong",
+               shard="seq"),
     "c4": dict(workload="Qwen3-14B shape (40L, 40q/8kv, d128, bf16) b=64 ctx 32K budget 2K",
                L=40, m=40, g=8, d=128, batch=64, ctx=32768, k=2048, delta=[2, 6, 35], F=2, scaling="strong"),
 }
@@ -233,21 +235,29 @@ def run_ours(args, c):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
-    if c["scaling"] == "weak":
+    seq_shard = c.get("shard") == "seq" and world > 1
+    if c["scaling"] == "weak" or seq_shard:
         batch = c["batch"]
     else:
         batch = max(1, c["batch"] // world)
+    nccl_ids = [None, None]
+    if seq_shard:  # rank 0 creates one NCCL id per handle (DELTA stack, Full stack); all ranks join
+        obj = [[d200.nccl_unique_id(), d200.nccl_unique_id()] if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_ids = obj[0]
     W, K = args.warmup, args.steps
     s_first = c["ctx"]                        # s after the append of the first timed step
     s_pre = s_first - W - 1                   # tokens in the cache before warm-up
     max_seq = s_first + K + PAGE
-    seed = 2511 + 1000 * rank
+    seed = 2511 if seq_shard else 2511 + 1000 * rank  # batch sharding: every rank its own sequences
 
     def make_cfg(full: bool):
         return d200.DeltaConfig(num_layers=c["L"], num_q_heads=c["m"], num_kv_heads=c["g"], head_dim=c["d"],
                                 max_batch=batch, max_seq_len=max_seq,
                                 num_full_prefix=c["L"] if full else c["F"], select_layers=[] if full else c["delta"],
-                                budget_k=c["k"], n_sink=S_SINK, n_window=L_WIN, select_block=PAGE)
+                                budget_k=c["k"], n_sink=S_SINK, n_window=L_WIN, select_block=PAGE,
+                                shard_world=world if seq_shard else 1, shard_rank=rank if seq_shard else 0,
+                                nccl_id=nccl_ids[1 if full else 0])
 
     cfg = make_cfg(False)
     bt = torch.from_numpy(synth.block_table(seed, batch, cfg.max_pages))
@@ -327,7 +337,7 @@ def run_ours(args, c):
         sb = step_bytes(c, s, batch, sparse_token_count(s, c["k"]))
         byts_delta += sb["delta"]
         byts_full += sb["full_stack"]
-    tot_delta = byts_delta * world
+    tot_delta = byts_delta * (1 if seq_shard else world)  # sequence sharding: one sequence in total
     value = tot_delta / (ms_delta * 1e-3) / 1e9
 
     # ---- e2e through delta_decode_step_host (pinned host buffers, copies inside the region)
@@ -427,14 +437,14 @@ def run_ours(args, c):
         "config": {"workload": c["workload"], "per_rank_batch": batch, "global_batch": batch * world,
                    "context": f"s = {s_first}..{s_first + K - 1} tokens after append (grows 1/step)",
                    "budget_k": c["k"], "n_sink": S_SINK, "n_window": L_WIN, "select_block": PAGE,
-                   "delta_layers": c["delta"], "full_prefix": c["F"], "parallelism": f"batch-shard x{world}",
+                   "delta_layers": c["delta"], "full_prefix": c["F"], "parallelism": (f"sequence-shard x{world} (NCCL)" if seq_shard else f"batch-shard x{world}"),
                    "l2": "inputs larger than L2: >= 861 MB of KV read per step vs 126 MB L2 (no flush)"},
         "decode_step_us": round(1e3 * ms_delta / K, 2),
         "full_stack_us": round(1e3 * ms_full / K, 2),
         "speedup_vs_full": round(ms_full / ms_delta, 3),
         "byte_ratio": round(byte_ratio, 3),
         "speedup_target": round(0.8 * byte_ratio, 3),
-        "full_stack_gbs": round(byts_full * world / (ms_full * 1e-3) / 1e9, 2),
+        "full_stack_gbs": round(byts_full * (1 if seq_shard else world) / (ms_full * 1e-3) / 1e9, 2),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": "attn_tc_kernel<128,false> FULL, one layer, s=%d" % s_last,

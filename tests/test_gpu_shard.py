@@ -116,3 +116,11 @@ def test_shard_with_empty_rank():
     outs, _, plans = sharded.step(q, k, v)
     np.testing.assert_allclose(outs[0], out_u, atol=1e-5, rtol=0)
     assert plans[1][3][0].tolist() == plans_u[1][0].tolist()
+
+
+def test_nccl_loads_and_makes_an_id():
+    """The NCCL path loads the library at run time (the copy torch uses) and produces an id;
+    the multi-GPU exchange itself needs >= 2 GPUs (bench.py --config c3 under torchrun)."""
+    import paper_2510_09883_b200 as d200
+    uid = d200.nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128 and any(uid)
