@@ -393,11 +393,12 @@ size_t select_smem_bytes(int max_units) {
 
 cudaError_t launch_select(const SelectParams& p, cudaStream_t st, bool pdl) {
     const size_t smem = select_smem_bytes(p.max_units);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && configured < smem) {
-        cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static bool configured = false;  // static + dynamic shared memory exceeds the 48 KiB default
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)select_smem_bytes(kSmemUnits));
         if (e != cudaSuccess) return e;
-        configured = smem;
+        configured = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.keys_override ? 1 : p.nchunk, p.batch);
