@@ -54,23 +54,12 @@ static_assert(kDeep % NGRP == 0 && kShallow % NGRP == 0, "ring slots must map to
 
 template <int D, int NSTAGE>
 struct TcCfg {
-    static constexpr int kHalf = kPage * D * 2;        // bytes of one head-page of K (or of V)
-    static constexpr int kTile = 2 * kHalf;            // K then V of one (page, head): one TMA request
+    static constexpr int kHalf = TileLayout<D>::kVOff;   // K rows -> V rows of a tile
+    static constexpr int kTile = TileLayout<D>::kBytes;  // K and V of one (page, head): one TMA request
     static constexpr int kRing = NSTAGE * NT * kTile;
     static constexpr int kRowTok = NSTAGE * NT * kPage;  // token id of every ring row (-1 = none)
     static constexpr int kSmem = 1024 + kRing + ClusterStage<D>::kBytes + 2 * NSTAGE * 8 + kRowTok * 4 + 16;
 };
-
-// Byte offset of 16-byte chunk c (0..D/8-1) of row r inside a 128B-swizzled head-page as
-// one TMA box writes it.  D = 64: 16 rows of 128 B.  D = 128: the box is 3-D {64, 2, 16}
-// (one 4 KiB request per head-page), so row r's two 128-byte halves are consecutive
-// 128-byte lines 2r and 2r+1; the 128B swizzle XORs the chunk with the line index mod 8.
-template <int D>
-__device__ __forceinline__ uint32_t swz(int r, int c) {
-    if (D == 64) return (uint32_t)(r * 128 + (((c & 7) ^ (r & 7)) << 4));
-    const int line = 2 * r + (c >> 3);
-    return (uint32_t)(line * 128 + (((c & 7) ^ (line & 7)) << 4));
-}
 
 template <int D, bool TOKEN_PLAN, int NSTAGE, int NH>
 __global__ void __launch_bounds__(kThreads, NH == 1 ? 2 : 1)  // two CTAs per SM (cluster residency)
@@ -199,7 +188,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
                         const int row0 = (int)kv_row(layer_ph + phys_w, p.g, h, 0);
                         uint8_t* dst = ring + (stg * NT + lane) * C::kTile;
                         if (D == 64) tma_load_2d(dst, &tm_kv, &full[stg], 0, row0, kEvictFirst);
-                        else tma_load_3d(dst, &tm_kv, &full[stg], 0, 0, row0, kEvictFirst);
+                        else tma_load_3d(dst, &tm_kv, &full[stg], 0, row0, 0, kEvictFirst);
                     }
                 }
             }

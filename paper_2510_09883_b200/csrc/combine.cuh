@@ -36,6 +36,23 @@ __device__ __forceinline__ void set_err(int32_t* err, int code) {
     if (err) atomicCAS(err, 0, code);
 }
 
+// Shared-memory image of one (page, kv head) tile as the TMA box {64, 2P rows, D/64 halves}
+// with SWIZZLE_128B writes it: [half][row][128 B]; rows 0..P-1 are K, rows P..2P-1 are V.
+// Each 64-element half of all 2P rows is a run of 128-byte lines (the canonical UMMA SW128
+// layout: K-major for K, MN-major for V).
+template <int D>
+struct TileLayout {
+    static constexpr int kHalfBytes = 2 * kPage * 128;    // 4096: one half of the 32 rows
+    static constexpr int kVOff = kPage * 128;             // 2048: first V row
+    static constexpr int kBytes = (D / 64) * kHalfBytes;  // 8192 (d = 128) / 4096 (d = 64)
+};
+// Byte offset of 16-byte chunk c (0..D/8-1) of row r (K rows from the tile base, V rows from
+// base + kVOff): the 128B swizzle XORs the chunk with the line index mod 8.
+template <int D>
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+    return (uint32_t)((c >> 3) * TileLayout<D>::kHalfBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+
 // Does this rank hold logical page u (sequence sharding; always true when unsharded)?
 __device__ __forceinline__ bool owns_page(const AttnParams& p, int u) { return u >= p.page_lo && u < p.page_hi; }
 

@@ -258,7 +258,10 @@ struct delta_ctx {
     uint64_t launches = 0;
     bool pdl = true;
     int tune_nsplit = 0, tune_deep = -1;  // DELTA_TUNE overrides (0 / -1 = automatic)
-    int tune_prewait = 1, tune_early = 1;
+    // tcgen05 kernel (attn_umma.cu): correct, but one tcgen05.mma of a 16-token tile costs ~48
+    // cycles to issue (tools/umma_test.cu), so 10 per tile lose to the mma.sync kernel here;
+    // kept selectable (DELTA_TUNE umma=1) and parity-tested.
+    int tune_prewait = 1, tune_early = 1, tune_umma = 0;
     // sequence sharding
     int world = 1, rank = 0, page_lo = 0, page_hi = 0x7fffffff;
     ncclComm_t comm = nullptr;  // null with world > 1: the caller exchanges (delta_shard_* calls)
@@ -387,8 +390,11 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
         p.prewait = 0;
     if (p.role == kRoleSparse && h->last_kind == delta_ctx::kLastSelect && h->last_layer == h->gov[layer])
         p.prewait = 0;
-    cudaError_t e = h->use_tc ? launch_attn_tc(p, &h->tm_kv, st, h->pdl)
-                              : launch_attn_simt(p, h->cfg.kv_dtype == DELTA_BF16, st, h->pdl);
+    // bf16: the tcgen05/TMEM kernel for GQA groups of <= 8 heads, the mma.sync kernel otherwise;
+    // fp32 caches: the CUDA-core kernel (no tensor-core rounding of fp32 inputs).
+    cudaError_t e = !h->use_tc ? launch_attn_simt(p, h->cfg.kv_dtype == DELTA_BF16, st, h->pdl)
+                    : (h->tune_umma && umma_supported(p)) ? launch_attn_umma(p, &h->tm_kv, st, h->pdl)
+                                                          : launch_attn_tc(p, &h->tm_kv, st, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "decode launch");
     ++h->launches;
     h->last_kind = delta_ctx::kLastAttn;
@@ -563,13 +569,14 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
         auto encode = reinterpret_cast<PFN_encodeTiled>(fn);
         // One box = one (page, head): its P K rows and P V rows (2P rows x d), i.e. one 4 KiB
         // (d = 64) or 8 KiB (d = 128) request.  d = 64: 2-D {64, rows}.  d = 128: 3-D
-        // {64, 2, rows} so a single request covers both 128-byte halves of each row under the
-        // 128B swizzle (the inner box extent is limited to 128 bytes).
+        // {64, rows, 2 halves} so a single request covers both 128-byte halves of each row under
+        // the 128B swizzle (inner box extent <= 128 bytes) and lands as [half][row][128 B], the
+        // canonical tcgen05 SW128 operand layout (combine.cuh TileLayout).
         const bool d128 = cfg->head_dim == 128;
         const cuuint32_t rank = d128 ? 3 : 2;
-        const cuuint64_t dims[3] = {64, d128 ? 2ull : (cuuint64_t)rows, (cuuint64_t)rows};
-        const cuuint64_t strides[2] = {128ull, 256ull};
-        const cuuint32_t box[3] = {64, d128 ? 2u : (cuuint32_t)(2 * kPage), (cuuint32_t)(2 * kPage)};
+        const cuuint64_t dims[3] = {64, (cuuint64_t)rows, 2};
+        const cuuint64_t strides[2] = {d128 ? 256ull : 128ull, 128ull};
+        const cuuint32_t box[3] = {64, (cuuint32_t)(2 * kPage), 2};
         const cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = encode(&h->tm_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, bufs->kv_pool, dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -613,6 +620,7 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
         if (d) h->tune_deep = std::atoi(d + 5);
         if (const char* w = std::strstr(t, "prewait=")) h->tune_prewait = std::atoi(w + 8);
         if (const char* w = std::strstr(t, "early=")) h->tune_early = std::atoi(w + 6);
+        if (const char* w = std::strstr(t, "umma=")) h->tune_umma = std::atoi(w + 5);
     }
     h->step.assign(cfg->num_layers, 0);
     h->dec_step.assign(cfg->num_layers, -1);

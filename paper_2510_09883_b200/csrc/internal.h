@@ -118,6 +118,8 @@ struct AppendParams {
 // Launchers (attn_tc.cu / attn_simt.cu / select.cu / append.cu).  Each returns the
 // cudaError_t of the launch.  `pdl` enables programmatic dependent launch.
 cudaError_t launch_attn_tc(const AttnParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl);
+cudaError_t launch_attn_umma(const AttnParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl);
+bool umma_supported(const AttnParams& p);
 cudaError_t launch_attn_simt(const AttnParams& p, bool bf16, cudaStream_t st, bool pdl);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t st, bool pdl);
 cudaError_t launch_append(const AppendParams& p, cudaStream_t st, bool pdl);

@@ -274,3 +274,30 @@ def test_c1_full_size_planted_graph_step():
     # Delta selections: known without the oracle
     units = set(synth.planted_units(2511, 2, 0, plant).tolist())
     assert set(ref[2][2].tolist()) == units | {0, 2046, 2047}   # sink page + 2 window pages
+
+
+# ---------------------------------------------------------------- tcgen05 / TMEM kernel (opt-in)
+
+@pytest.mark.parametrize("shape,s", [
+    (Shape(L=4, m=32, g=8, d=128, F=1, delta=[1], k=512, S=4, Lw=32, block=16, dtype="bf16"), 3001),   # gs 4
+    (Shape(L=3, m=28, g=4, d=128, F=1, delta=[1], k=1024, S=4, Lw=32, block=16, dtype="bf16"), 2101),  # gs 7
+    (Shape(L=3, m=16, g=2, d=64, F=1, delta=[1], k=64, S=4, Lw=32, block=1, dtype="bf16"), 2101),      # d 64, tokens
+], ids=["gs4", "gs7", "d64-token"])
+def test_umma_kernel_parity(shape, s, monkeypatch):
+    """The tcgen05.mma / TMEM decode kernel (attn_umma.cu, DELTA_TUNE umma=1) against the oracle."""
+    monkeypatch.setenv("DELTA_TUNE", "umma=1")
+    case = GpuCase(shape, 91, batch=2, s_pre=s - 1, max_seq=s + 64)
+    out, lse, plans = case.step_layers(s)
+    _check_step(case, s, out, lse, plans)
+
+
+def test_umma_fewhot_epochs(monkeypatch):
+    """Concentrated attention arriving late in the cache forces stabiliser raises (new TMEM
+    accumulator epochs) in the tcgen05 kernel; the result must still meet the bound."""
+    monkeypatch.setenv("DELTA_TUNE", "umma=1")
+    sh = Shape(L=2, m=32, g=8, d=128, F=2, delta=[], k=0, S=0, Lw=0, block=16, dtype="bf16")
+    plant = planting_for(Shape(L=2, m=32, g=8, d=128, F=2, delta=[], k=0, S=4, Lw=32, block=1, dtype="bf16"),
+                         4096, "fewhot")
+    case = GpuCase(sh, 8, batch=1, s_pre=4095, max_seq=4096, planting=plant)
+    out, lse, plans = case.step_layers(4096)
+    _check_step(case, 4096, out, lse, plans)

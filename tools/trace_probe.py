@@ -35,6 +35,9 @@ def read():
 def report(name, tr3):
     tr = tr3.reshape(-1, 12)
     live = tr[:, 0] > 0
+    if not live.any():
+        print(f"== {name}: no stamps (kernel from another translation unit)")
+        return
     t = tr[live]
     t0 = t[:, 0].min()
     rel = np.where(t > 0, t - t0, -1)
@@ -90,6 +93,9 @@ def main():
                     fn()
                 s.synchronize()
                 report(f"{name} rep {rep}", read())
+            if os.environ.get("PROBE_TILES"):
+                print(f"   tiles of {name}:")
+                tiles()
         # back-to-back: the step's own sequence, eager (timed with events too)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         with torch.cuda.stream(s):
@@ -147,6 +153,18 @@ def main():
             print(f"   L{l:2d}: {f(0, np.min):7.2f} {f(1, np.median):7.2f} {f(2, np.median):7.2f} "
                   f"{f(3, np.median):7.2f} {f(3, np.max):7.2f} {f(5, np.median):7.2f} {f(7, np.median):7.2f} "
                   f"{f(7, np.max):7.2f} {f(9, np.max):7.2f} {f(6, np.max):7.2f}")
+
+
+def tiles():
+    """Per-tile event times (us) of CTA (0,0,0) of the last traced umma launch."""
+    t = np.zeros(64 * 8, np.uint64)
+    assert lib.delta_trace_read_tiles(t.ctypes.data_as(ctypes.c_void_p)) == 0
+    t = t.reshape(64, 8).astype(np.int64)
+    t0 = t[0, 0]
+    print("   tile: tma_issued full_seen qk_issued s_seen p_done pv_issued (us from tile-0 TMA issue)")
+    for i in range(40):
+        r = [(x - t0) / 1e3 if x > 0 else float("nan") for x in t[i, :6]]
+        print(f"   {i:3d}: " + " ".join(f"{v:8.2f}" for v in r))
 
 
 if __name__ == "__main__":
