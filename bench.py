@@ -45,8 +45,9 @@ CONFIGS = {
                         "partial merge + global top-k candidate merge)",
                L=32, m=32, g=8, d=128, batch=1, ctx=131072, k=2048, delta=[2, 16, 25], F=2, scaling="strong",
                shard="seq"),
-    "c4": dict(workload="Qwen3-14B shape (40L, 40q/8kv, d128, bf16) b=64 ctx 32K budget 2K",
-               L=40, m=40, g=8, d=128, batch=64, ctx=32768, k=2048, delta=[2, 6, 35], F=2, scaling="strong"),
+    "c4": dict(workload="Qwen3-14B shape (40L, 40q/8kv, d128, bf16) ctx 32K budget 2K, 8 sequences per GPU "
+                        "(the 8xB200 config's per-GPU share of batch 64; 43 GB of KV per GPU)",
+               L=40, m=40, g=8, d=128, batch=8, ctx=32768, k=2048, delta=[2, 6, 35], F=2, scaling="weak"),
 }
 S_SINK, L_WIN, PAGE = 4, 32, 16
 

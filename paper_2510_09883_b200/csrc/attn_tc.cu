@@ -41,16 +41,18 @@ extern "C" int delta_trace_read(void* host, size_t bytes) {  // copies then clea
 namespace delta {
 namespace {
 
-constexpr int NT = 3;            // tiles per ring stage
-constexpr int NGRP = 2;          // consumer groups; ring slot i is always consumed by group i % NGRP
-constexpr int NCW = NT * NGRP;   // consumer warps (more than one per SM sub-partition: latency hiding)
+constexpr int NT = 3;            // tiles per ring stage; a group of NT consumer warps takes a stage
 constexpr int kBatch = (32 / NT) * NT;  // tiles whose page ids the producer resolves at once
-constexpr int kThreads = (NCW + 1) * 32;
-// pipeline depth in stages of NT head-pages: kDeep when one CTA per SM, kShallow when two CTAs
-// share an SM.  Must be a multiple of NGRP: a group then always consumes the same slots, in
-// consecutive rounds, so its mbarrier parity waits can never alias a round it skipped.
+// Consumer groups NG (ring slot i is always consumed by group i % NG) and ring depth NSTAGE
+// (stages of NT tiles; a multiple of NG, so a group consumes the same slots in consecutive
+// rounds and its mbarrier parity waits can never alias a round it skipped):
+//  * full-cache layers: NG = 2 (6 consumer warps), NSTAGE = 4 (96 KiB in flight) — or 8 with
+//    one CTA per SM (deep);
+//  (NG = 3 with NSTAGE = 3 — nine warps, one tile each for a sparse layer's ~8 tiles per CTA —
+//  measured no faster at C1: the sparse layer is bound by its fixed latencies.)
 constexpr int kDeep = 8, kShallow = 4;
-static_assert(kDeep % NGRP == 0 && kShallow % NGRP == 0, "ring slots must map to fixed consumer groups");
+template <int NG>
+constexpr int cta_threads() { return (NT * NG + 1) * 32; }
 
 template <int D, int NSTAGE>
 struct TcCfg {
@@ -61,9 +63,12 @@ struct TcCfg {
     static constexpr int kSmem = 1024 + kRing + ClusterStage<D>::kBytes + 2 * NSTAGE * 8 + kRowTok * 4 + 16;
 };
 
-template <int D, bool TOKEN_PLAN, int NSTAGE, int NH>
-__global__ void __launch_bounds__(kThreads, NH == 1 ? 2 : 1)  // two CTAs per SM (cluster residency)
+template <int D, bool TOKEN_PLAN, int NSTAGE, int NH, int NG>
+__global__ void __launch_bounds__(cta_threads<NG>(), NH == 1 ? 2 : 1)  // two CTAs per SM (cluster residency)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
+    static_assert(NSTAGE % NG == 0, "ring slots must map to fixed consumer groups");
+    constexpr int NCW = NT * NG;  // consumer warps; warp NCW is the producer
+    constexpr int NGRP = NG;
     using C = TcCfg<D, NSTAGE>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -135,7 +140,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     float* ms = reinterpret_cast<float*>(ring);
     float* ls = ms + NCW * 16;
     float* os = ls + NCW * 16;
-    static_assert((2 * NCW * 16 + NCW * 16 * os_stride<D>()) * 4 <= TcCfg<D, NSTAGE>::kRing,
+    constexpr int OSR = 8 * NH;  // O rows kept per warp (the group's heads, gs <= 8 * NH)
+    static_assert((2 * NCW * 16 + NCW * OSR * os_stride<D>()) * 4 <= TcCfg<D, NSTAGE>::kRing,
                   "epilogue state must fit in the K ring");
 
     if (warp == NCW) {
@@ -453,21 +459,22 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
                 for (int i = 0; i < 4; ++i) {
                     const int hq = nh * 8 + 2 * t4 + (i & 1);
                     const int dd = mt * 16 + g4 + 8 * (i >> 1);
-                    if (hq < gs) os[(warp * 16 + hq) * os_stride<D>() + dd] = o[nh][mt][i];
+                    if (hq < gs) os[(warp * OSR + hq) * os_stride<D>() + dd] = o[nh][mt][i];
                 }
         }
     }
     __syncthreads();  // producer joins: warp states complete
     if (!p.early_trigger) pdl_launch_dependents();
     if (tid == 0) DTRACE(4);
-    cluster_epilogue<D, NCW>(p, ms, ls, os, cstage, b, h, stale, cap_err, s);
+    cluster_epilogue<D, NCW, OSR>(p, ms, ls, os, cstage, b, h, stale, cap_err, s);
     if (tid == 0) DTRACE(6);
 }
 
-template <int D, bool TOKEN_PLAN, int NST, int NH>
+template <int D, bool TOKEN_PLAN, int NST, int NH, int NG>
 cudaError_t launch_impl(const AttnParams& p0, const CUtensorMap* tm_kv,
                         cudaStream_t st, bool pdl) {
-    auto kern = attn_tc_kernel<D, TOKEN_PLAN, NST, NH>;
+    auto kern = attn_tc_kernel<D, TOKEN_PLAN, NST, NH, NG>;
+    constexpr int kThreads = cta_threads<NG>();
     constexpr int smem = TcCfg<D, NST>::kSmem;
     static int max_cluster = 0;  // largest feasible cluster for this instantiation
     if (max_cluster == 0) {
@@ -499,10 +506,10 @@ template <int D, bool TOKEN_PLAN>
 cudaError_t launch_stages(const AttnParams& p, const CUtensorMap* tm_kv, cudaStream_t st,
                           bool pdl) {
     if (p.gs <= 8)
-        return p.deep ? launch_impl<D, TOKEN_PLAN, kDeep, 1>(p, tm_kv, st, pdl)
-                      : launch_impl<D, TOKEN_PLAN, kShallow, 1>(p, tm_kv, st, pdl);
-    return p.deep ? launch_impl<D, TOKEN_PLAN, kDeep, 2>(p, tm_kv, st, pdl)
-                  : launch_impl<D, TOKEN_PLAN, kShallow, 2>(p, tm_kv, st, pdl);
+        return p.deep ? launch_impl<D, TOKEN_PLAN, kDeep, 1, 2>(p, tm_kv, st, pdl)
+                      : launch_impl<D, TOKEN_PLAN, kShallow, 1, 2>(p, tm_kv, st, pdl);
+    return p.deep ? launch_impl<D, TOKEN_PLAN, kDeep, 2, 2>(p, tm_kv, st, pdl)
+                  : launch_impl<D, TOKEN_PLAN, kShallow, 2, 2>(p, tm_kv, st, pdl);
 }
 
 }  // namespace
@@ -510,13 +517,13 @@ cudaError_t launch_stages(const AttnParams& p, const CUtensorMap* tm_kv, cudaStr
 #ifdef DELTA_TRACE
 // trace builds: max co-resident clusters of the real kernel for a cluster size
 extern "C" int delta_debug_cluster_occupancy(int deep, int cs) {
-    auto kern = deep ? attn_tc_kernel<128, false, kDeep, 1> : attn_tc_kernel<128, false, kShallow, 1>;
+    auto kern = deep ? attn_tc_kernel<128, false, kDeep, 1, 2> : attn_tc_kernel<128, false, kShallow, 1, 2>;
     const int smem = deep ? TcCfg<128, kDeep>::kSmem : TcCfg<128, kShallow>::kSmem;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs, 8, 1);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(cta_threads<2>());
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute a;
     a.id = cudaLaunchAttributeClusterDimension;

@@ -83,7 +83,7 @@ __device__ __forceinline__ void split_geometry(const AttnParams& p, int b, int s
 // cluster = the `nsplit` CTAs of one (sequence, kv head); rank = split).  Push model, one
 // cluster barrier:
 //  1. each thread folds the warps' states (ms[w*16+row] running max in log2 units, ls
-//     running sum, os[(w*16+row)*OS+col] unnormalised O) in fixed warp order into this CTA's
+//     running sum, os[(w*OSROWS+row)*OS+col] unnormalised O) in fixed warp order into this CTA's
 //     (M_c, L_c, O_c) for its float4 of the gs x D output, and stores it straight into the
 //     shared staging of the CTA that owns that output slice (distributed shared memory);
 //  2. cluster barrier (release / acquire): every pushed value is visible to its owner;
@@ -97,7 +97,7 @@ __device__ __forceinline__ void split_geometry(const AttnParams& p, int b, int s
 // Length counter encoding: seq_len_raw[l][b] = n * g.  Each of the g head clusters of a
 // fused append+decode adds 1 when it is done; every reader takes raw / g, which is exact
 // because a reader's own cluster has not yet added, so at most g - 1 additions precede it.
-template <int D, int NW>
+template <int D, int NW, int OSROWS = 16>
 __device__ __forceinline__ void cluster_epilogue(const AttnParams& p, const float* ms, const float* ls,
                                                  const float* os, float* stage, int b, int h, bool stale,
                                                  bool cap_err, int s_post) {
@@ -122,7 +122,7 @@ __device__ __forceinline__ void cluster_epilogue(const AttnParams& p, const floa
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
             mw[w] = ms[w * 16 + row];
-            v[w] = reinterpret_cast<const float4*>(os + (w * 16 + row) * OS)[c4];
+            v[w] = reinterpret_cast<const float4*>(os + (w * OSROWS + row) * OS)[c4];
         }
         float M = mw[0];
 #pragma unroll

@@ -43,11 +43,13 @@ int num_sms_current() {
     return sms > 0 ? sms : 148;
 }
 
-// Split-K CTAs per (sequence, kv head) = cluster size: about two CTAs per SM in total (the
-// shallow-ring kernel fits two per SM), at most 16 (one cluster).
+// Split-K CTAs per (sequence, kv head) = cluster size: as many as fit in ONE wave of two CTAs
+// per SM (the shallow-ring kernel fits two per SM), at most 16 (one cluster).  Rounding down
+// matters: at batch 8 x 8 heads, 5 splits (320 CTAs > 296 slots) leave a second, under-occupied
+// wave — measured 190 us vs 161 us for 4 splits on a 32K full layer, 25 vs 18 us sparse.
 int nsplit_full(int batch, int g, int sms, int max_pages) {
     const int heads = std::max(1, batch * g);
-    int n = (2 * sms + heads - 1) / heads;
+    int n = (2 * sms) / heads;
     n = std::max(1, std::min(n, kMaxSplit));
     return std::min(n, std::max(1, max_pages));
 }
@@ -258,6 +260,7 @@ struct delta_ctx {
     uint64_t launches = 0;
     bool pdl = true;
     int tune_nsplit = 0, tune_deep = -1;  // DELTA_TUNE overrides (0 / -1 = automatic)
+    int tune_snsplit = 0;                 // sparse layers only
     // tcgen05 kernel (attn_umma.cu): correct, but one tcgen05.mma of a 16-token tile costs ~48
     // cycles to issue (tools/umma_test.cu), so 10 per tile lose to the mma.sync kernel here;
     // kept selectable (DELTA_TUNE umma=1) and parity-tested.
@@ -322,6 +325,7 @@ AttnParams attn_params(delta_ctx* h, int layer, int batch) {
         }
     }
     if (h->tune_nsplit > 0) p.nsplit = std::min(h->tune_nsplit, kMaxSplit);
+    if (h->tune_snsplit > 0 && p.role == kRoleSparse) p.nsplit = std::min(h->tune_snsplit, kMaxSplit);
     p.deep = deep_ring(batch, c.num_kv_heads, p.nsplit, h->sms) ? 1 : 0;
     if (h->tune_deep >= 0) p.deep = h->tune_deep;
     return p;
@@ -615,10 +619,12 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
     // Tuning hook for kernel experiments (tools/trace_probe.py): DELTA_TUNE="nsplit=N,deep=0|1".
     if (const char* t = std::getenv("DELTA_TUNE")) {
         const char* a = std::strstr(t, "nsplit=");
+        while (a && a != t && a[-1] != ',') a = std::strstr(a + 1, "nsplit=");  // not "snsplit="
         const char* d = std::strstr(t, "deep=");
         if (a) h->tune_nsplit = std::atoi(a + 7);
         if (d) h->tune_deep = std::atoi(d + 5);
         if (const char* w = std::strstr(t, "prewait=")) h->tune_prewait = std::atoi(w + 8);
+        if (const char* w = std::strstr(t, "snsplit=")) h->tune_snsplit = std::atoi(w + 8);
         if (const char* w = std::strstr(t, "early=")) h->tune_early = std::atoi(w + 6);
         if (const char* w = std::strstr(t, "umma=")) h->tune_umma = std::atoi(w + 5);
     }

@@ -32,6 +32,20 @@ def read():
     return a.copy()
 
 
+def per_cluster(tr3, nsplit=16, slot=3):
+    """loop-done spread per cluster (head) of one layer's trace: is the skew per GPC or per CTA?"""
+    t = tr3.reshape(-1, 12)
+    live = t[:, 0] > 0
+    if not live.any():
+        return
+    t0 = t[live, 0].min()
+    n = int(live.sum())
+    for hd in range(n // nsplit):
+        v = (t[hd * nsplit:(hd + 1) * nsplit, slot] - t0) / 1e3
+        print(f"      head {hd}: loop done min {v.min():6.2f} med {np.median(v):6.2f} max {v.max():6.2f}  "
+              f"argmax split {int(v.argmax())}")
+
+
 def report(name, tr3):
     tr = tr3.reshape(-1, 12)
     live = tr[:, 0] > 0
@@ -92,7 +106,10 @@ def main():
                 with torch.cuda.stream(s):
                     fn()
                 s.synchronize()
-                report(f"{name} rep {rep}", read())
+                tr_ = read()
+                report(f"{name} rep {rep}", tr_)
+                if os.environ.get("PROBE_CLUSTERS"):
+                    per_cluster(tr_[0] if name.startswith("FULL") else tr_[3])
             if os.environ.get("PROBE_TILES"):
                 print(f"   tiles of {name}:")
                 tiles()
