@@ -27,11 +27,17 @@ __global__ void __launch_bounds__(NW * 32) attn_simt_kernel(const AttnParams p) 
     constexpr int VPL = D / 32;
     __shared__ float ms[NW * 16], ls[NW * 16];
     __shared__ __align__(16) float os[NW * 16 * os_stride<D>()];
-    __shared__ __align__(16) float cstage[ClusterStage<D>::kFloats];  // peers push partials here
+    __shared__ __align__(16) float cstage[ClusterStage<D>::kBytes / 4];  // peers push partials here
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int gs = p.gs;
+    if (tid == 0) {
+        cluster_stage_init<D>(cstage, gs);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    cluster_arrive_relaxed();
     pdl_wait();
     pdl_launch_dependents();  // after the wait: the next kernel may launch (see attn_tc.cu)
 

@@ -87,12 +87,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
             mbar_init(&full[i], TOKEN_PLAN ? 32 : 1);
             mbar_init(&empty[i], NT);
         }
+        cluster_stage_init<D>(cstage, p.gs);
         fence_mbar_init();
     }
     if (!TOKEN_PLAN && warp == NCW && lane == 0) {
         tma_prefetch_desc(&tm_kv);
     }
     __syncthreads();
+    cluster_arrive_relaxed();  // peers may push into cstage once they pass the matching wait
     if (tid == 0) DTRACE(0);
     // Programmatic dependent launch: without `prewait` everything waits for the previous
     // kernel here.  With `prewait` (the host knows the previous kernel of this handle wrote
@@ -437,7 +439,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
 
         // ---------------------------------------------------------------- warp states
         if (tid == 0) DTRACE(3);
+        if (tid == (NCW - 1) * 32) DTRACE(11);
         consumer_bar(NCW * 32);  // every consumer is done reading the ring
+        if (tid == 0) DTRACE(8);
 #pragma unroll
         for (int nh = 0; nh < NH; ++nh) {
             if (nh >= nh_used) continue;
@@ -463,6 +467,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
                 }
         }
     }
+    if (tid == 0) DTRACE(10);
     __syncthreads();  // producer joins: warp states complete
     if (!p.early_trigger) pdl_launch_dependents();
     if (tid == 0) DTRACE(4);

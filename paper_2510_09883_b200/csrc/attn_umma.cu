@@ -137,6 +137,7 @@ attn_umma_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) 
             mbar_init(&p_free[i], 1);
         }
         mbar_init(o_done, 1);
+        cluster_stage_init<D>(cstage, gs);
         fence_mbar_init();
     }
     if (!TOKEN_PLAN && warp == 2 && lane == 0) tma_prefetch_desc(&tm_kv);
@@ -148,6 +149,7 @@ attn_umma_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    cluster_arrive_relaxed();
     const uint32_t tbase = *tmem_slot;
     if (tid == 0) DTRACE(0);
     if (!p.prewait) pdl_wait();

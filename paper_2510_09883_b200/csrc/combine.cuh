@@ -5,8 +5,6 @@
 // Within a CTA, each warp keeps an online-softmax state (running max m in log2 units,
 // running sum l, unnormalised O) over the tokens it processed.
 #pragma once
-#include <cooperative_groups.h>
-
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -19,9 +17,67 @@ constexpr float kLn2 = 0.6931471805599453f;
 template <int D>
 struct ClusterStage {
     static constexpr int kO4 = 16 * D / 4 + kMaxSplit;            // float4 slots: sO[rank * per + k]
-    static constexpr int kFloats = kO4 * 4 + 2 * kMaxSplit * 16;  // + sM[rank][16], sL[rank][16]
-    static constexpr int kBytes = kFloats * 4;
+    static constexpr int kFloats = kO4 * 4 + 2 * kMaxSplit * 16;  // + (M, L) pairs [rank][16]
+    static constexpr int kBarOff = kFloats * 4;                   // + the arrival mbarrier (8 B)
+    static constexpr int kBytes = kBarOff + 16;
 };
+
+__device__ __forceinline__ uint32_t cluster_nranks() {
+    uint32_t n;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
+    return n;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// Address of the same shared variable in cluster CTA `rank` (shared::cluster window).
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+// Remote stores that complete bytes on the destination CTA's mbarrier: no fence and no
+// cluster barrier on the push path (the owner waits on its own mbarrier for the bytes).
+__device__ __forceinline__ void st_async_v4(uint32_t dst, float4 v, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
+                 ::"r"(dst), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t dst, float a, float b, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];"
+                 ::"r"(dst), "f"(a), "f"(b), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+// Output slice of the gs x D float4s that cluster rank `r` merges: [r * per, min(total, (r + 1) * per)).
+struct EpiSlice {
+    int total, per, lo, n4, rows;
+    __device__ EpiSlice(int gs, int c4s, int ns, int r) {
+        total = gs * c4s;
+        per = (total + ns - 1) / ns;
+        lo = r * per;
+        n4 = max(0, min(total, lo + per) - lo);
+        rows = n4 > 0 ? (lo + n4 - 1) / c4s - lo / c4s + 1 : 0;
+    }
+};
+
+// Kernel prologue half of the cluster epilogue (thread 0, with the kernel's other mbarrier
+// inits, before fence_mbar_init): the arrival barrier expects, from each of the ns ranks, one
+// float4 per owned output element and one (M, L) pair per owned row.
+template <int D>
+__device__ __forceinline__ void cluster_stage_init(float* stage, int gs) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage) + ClusterStage<D>::kBarOff);
+    const int ns = (int)cluster_nranks();
+    const EpiSlice sl(gs, D / 4, ns, (int)cluster_rank());
+    mbar_init(bar, 1);
+    mbar_arrive_expect_tx(bar, (uint32_t)(ns * (sl.n4 * 16 + sl.rows * 8)));
+}
 
 // Row stride (floats) of the per-warp O states: D + 4 makes the fragment-order stores of
 // the MMA accumulators bank-conflict free and keeps float4 rows aligned.
@@ -80,18 +136,21 @@ __device__ __forceinline__ void split_geometry(const AttnParams& p, int b, int s
 }
 
 // Cluster split-K epilogue, called by EVERY thread of every CTA of the cluster (the
-// cluster = the `nsplit` CTAs of one (sequence, kv head); rank = split).  Push model, one
-// cluster barrier:
+// cluster = the `nsplit` CTAs of one (sequence, kv head); rank = split).  Push model over
+// st.async: the kernel called cluster_stage_init (thread 0) and cluster_arrive_relaxed (all
+// threads, after its __syncthreads) at entry, so every peer's arrival mbarrier is live by now.
 //  1. each thread folds the warps' states (ms[w*16+row] running max in log2 units, ls
 //     running sum, os[(w*OSROWS+row)*OS+col] unnormalised O) in fixed warp order into this CTA's
-//     (M_c, L_c, O_c) for its float4 of the gs x D output, and stores it straight into the
-//     shared staging of the CTA that owns that output slice (distributed shared memory);
-//  2. cluster barrier (release / acquire): every pushed value is visible to its owner;
-//  3. the owner of a slice merges the ns partials from its own shared memory in ascending
-//     rank order: M = max_c M_c, w_c = exp2(M_c - M), L = sum_c w_c L_c,
-//     O = sum_c w_c O_c / L, LSE = (M + log2 L) ln 2 — the identity that any partition of
-//     the attended token set gives the same softmax (Eq.4).  Fixed order:
-//     deterministic.  No CTA touches a peer's memory after the barrier.
+//     (M_c, L_c, O_c) for its float4 of the gs x D output and st.async-stores it straight into
+//     the shared staging of the CTA that owns that output slice; the thread holding a row's
+//     first float4 in an owner's range also sends the row's (M_c, L_c) pair;
+//  2. the owner waits on its own arrival mbarrier until all ns ranks' bytes have landed (no
+//     cluster barrier, no GPU-scope fence), then merges the ns partials in ascending rank
+//     order: M = max_c M_c, w_c = exp2(M_c - M), L = sum_c w_c L_c, O = sum_c w_c O_c / L,
+//     LSE = (M + log2 L) ln 2 — the identity that any partition of the attended token set
+//     gives the same softmax (Eq.4).  Fixed order: deterministic.
+//  A CTA exits once its own slice is written: nobody writes into its shared memory after its
+//  barrier completed (the expected byte count is exact), and it never reads a peer's.
 //  Rank 0 then reports device errors and, for a fused append, adds 1 to the length counter.
 //
 // Length counter encoding: seq_len_raw[l][b] = n * g.  Each of the g head clusters of a
@@ -101,20 +160,18 @@ template <int D, int NW, int OSROWS = 16>
 __device__ __forceinline__ void cluster_epilogue(const AttnParams& p, const float* ms, const float* ls,
                                                  const float* os, float* stage, int b, int h, bool stale,
                                                  bool cap_err, int s_post) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
     const int tid = threadIdx.x, nthreads = blockDim.x;
     const int gs = p.gs;
-    const int ns = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+    const int ns = (int)cluster_nranks(), rank = (int)cluster_rank();
     constexpr int C4 = D / 4, OS = os_stride<D>();
-    const int total = gs * C4;
-    const int per = (total + ns - 1) / ns;
+    const EpiSlice mine(gs, C4, ns, rank);
+    const int total = mine.total, per = mine.per;
     float4* sO = reinterpret_cast<float4*>(stage);
-    float* sM = stage + ClusterStage<D>::kO4 * 4;
-    float* sL = sM + kMaxSplit * 16;
-    // 1. push: each thread folds the NW warp states of one float4 (fixed warp order, fully
-    //    unrolled so every shared load is in flight at once) and stores it into the owner's
-    //    staging; the c4 == 0 thread of a row also pushes the row's (M_c, L_c) to every owner.
+    float* sM = stage + ClusterStage<D>::kO4 * 4;  // float2 (M_c, L_c) per [rank][row]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage) + ClusterStage<D>::kBarOff);
+    const uint32_t sO_u = smem_u32(sO), sM_u = smem_u32(sM), bar_u = smem_u32(bar);
+    cluster_wait();  // pairs with the entry arrive: every peer's barrier is initialised
+    // 1. push
     for (int idx = tid; idx < total; idx += nthreads) {
         const int row = idx / C4, c4 = idx - row * C4;
         float mw[NW];
@@ -135,66 +192,67 @@ __device__ __forceinline__ void cluster_epilogue(const AttnParams& p, const floa
             o.x += f[w] * v[w].x; o.y += f[w] * v[w].y; o.z += f[w] * v[w].z; o.w += f[w] * v[w].w;
         }
         const int r = idx / per, k = idx - r * per;
-        cl.map_shared_rank(sO, r)[rank * per + k] = o;
-        if (c4 == 0) {
+        const uint32_t rbar = mapa_u32(bar_u, (uint32_t)r);
+        st_async_v4(mapa_u32(sO_u + (uint32_t)(rank * per + k) * 16u, (uint32_t)r), o, rbar);
+        if (c4 == 0 || k == 0) {  // first float4 of this row in owner r's range: r needs (M, L)
             float L = 0.f;
 #pragma unroll
             for (int w = 0; w < NW; ++w) L += ls[w * 16 + row] * f[w];
-            for (int rr = 0; rr < ns; ++rr) {
-                cl.map_shared_rank(sM, rr)[rank * 16 + row] = M;
-                cl.map_shared_rank(sL, rr)[rank * 16 + row] = L;
-            }
+            st_async_v2(mapa_u32(sM_u + (uint32_t)(rank * 16 + row) * 8u, (uint32_t)r), M, L, rbar);
         }
     }
     if (tid == 0) DTRACE(5);
-    cl.sync();  // release / acquire: every pushed value is visible to its owner
-    if (tid == 0) DTRACE(7);
     // 2. owner: 16 lanes per owned float4, lane c holds rank c's partial; max, weights and
     //    sums are fixed shuffle trees over the 16 lanes (deterministic).
     bool bad = false;
-    const int grp = tid >> 4, c = tid & 15, ngrp = nthreads >> 4;
-    for (int k0 = 0; k0 < per; k0 += ngrp) {
-        const int k = k0 + grp;
-        const int idx = rank * per + k;
-        const bool live = k < per && idx < total;
-        const int row = live ? idx / C4 : 0, c4 = live ? idx - row * C4 : 0;
-        const bool mine = live && c < ns;
-        float mc = mine ? sM[c * 16 + row] : -INFINITY;
-        float lc = mine ? sL[c * 16 + row] : 0.f;
-        float4 x = mine ? sO[c * per + k] : make_float4(0.f, 0.f, 0.f, 0.f);
-        float M = mc;
+    if (mine.n4 > 0) {
+        mbar_wait(bar, 0);
+        if (tid == 0) DTRACE(7);
+        const int grp = tid >> 4, c = tid & 15, ngrp = nthreads >> 4;
+        const float2* sML = reinterpret_cast<const float2*>(sM);
+        for (int k0 = 0; k0 < per; k0 += ngrp) {
+            const int k = k0 + grp;
+            const int idx = rank * per + k;
+            const bool live = k < per && idx < total;
+            const int row = live ? idx / C4 : 0, c4 = live ? idx - row * C4 : 0;
+            const bool have = live && c < ns;
+            const float2 ml = have ? sML[c * 16 + row] : make_float2(-INFINITY, 0.f);
+            const float mc = ml.x, lc = ml.y;
+            float4 x = have ? sO[c * per + k] : make_float4(0.f, 0.f, 0.f, 0.f);
+            float M = mc;
 #pragma unroll
-        for (int off = 8; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-        const float f = (M == -INFINITY || mc == -INFINITY) ? 0.f : exp2f(mc - M);
-        float L = f * lc;
-        float4 v = make_float4(f * x.x, f * x.y, f * x.z, f * x.w);
+            for (int off = 8; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+            const float f = (M == -INFINITY || mc == -INFINITY) ? 0.f : exp2f(mc - M);
+            float L = f * lc;
+            float4 v = make_float4(f * x.x, f * x.y, f * x.z, f * x.w);
 #pragma unroll
-        for (int off = 8; off > 0; off >>= 1) {
-            L += __shfl_xor_sync(0xffffffffu, L, off);
-            v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
-            v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
-            v.z += __shfl_xor_sync(0xffffffffu, v.z, off);
-            v.w += __shfl_xor_sync(0xffffffffu, v.w, off);
-        }
-        if (live && c == 0) {
-            const float inv = (L > 0.f) ? 1.f / L : 0.f;
-            float4 o = make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv);
-            if (stale) {
-                const float qn = __int_as_float(0x7fc00000);  // NaN: stale plan must be loud
-                o = make_float4(qn, qn, qn, qn);
-            } else if (!(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w))) {
-                bad = true;
+            for (int off = 8; off > 0; off >>= 1) {
+                L += __shfl_xor_sync(0xffffffffu, L, off);
+                v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+                v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+                v.z += __shfl_xor_sync(0xffffffffu, v.z, off);
+                v.w += __shfl_xor_sync(0xffffffffu, v.w, off);
             }
-            const int j = h * gs + row;
-            const bool shard = p.shard_world > 1;  // the rank's partial; shard.cu merges the ranks
-            reinterpret_cast<float4*>((shard ? p.part_o : p.out) + ((size_t)b * p.m + j) * D)[c4] = o;
-            if (c4 == 0) {
-                const float lse = (L > 0.f) ? (M + log2f(L)) * kLn2 : -INFINITY;
-                if (shard) {
-                    p.part_lse[(size_t)b * p.m + j] = lse;
-                } else {
-                    if (p.lse_out) p.lse_out[(size_t)b * p.m + j] = lse;
-                    if (p.role == kRoleSelect) p.lse_buf[(size_t)b * p.m + j] = lse;
+            if (live && c == 0) {
+                const float inv = (L > 0.f) ? __frcp_rn(L) : 0.f;
+                float4 o = make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv);
+                if (stale) {
+                    const float qn = __int_as_float(0x7fc00000);  // NaN: stale plan must be loud
+                    o = make_float4(qn, qn, qn, qn);
+                } else if (!(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w))) {
+                    bad = true;
+                }
+                const int j = h * gs + row;
+                const bool shard = p.shard_world > 1;  // the rank's partial; shard.cu merges the ranks
+                reinterpret_cast<float4*>((shard ? p.part_o : p.out) + ((size_t)b * p.m + j) * D)[c4] = o;
+                if (c4 == 0) {
+                    const float lse = (L > 0.f) ? (M + log2f(L)) * kLn2 : -INFINITY;
+                    if (shard) {
+                        p.part_lse[(size_t)b * p.m + j] = lse;
+                    } else {
+                        if (p.lse_out) p.lse_out[(size_t)b * p.m + j] = lse;
+                        if (p.role == kRoleSelect) p.lse_buf[(size_t)b * p.m + j] = lse;
+                    }
                 }
             }
         }

@@ -58,9 +58,10 @@ def report(name, tr3):
     n = len(t)
     last = rel[:, 5] >= 0
     print(f"== {name}: {n} CTAs, span {(t[t > 0].max() - t0) / 1e3:.2f} us")
-    for k, lab in [(0, "entry"), (1, "pdl_wait done"), (2, "first stage landed"), (3, "loop done"),
-                   (4, "epilogue start"), (5, "cta merge done"), (7, "cluster sync 1"), (8, "peer M/L gathered"),
-                   (9, "outputs written"), (10, "cluster sync 2"), (6, "epilogue done")]:
+    for k, lab in [(0, "entry"), (1, "pdl_wait done"), (2, "first stage landed"), (3, "loop done w0"),
+                   (11, "loop done w_last"), (8, "consumer bar"), (10, "states written"),
+                   (4, "epilogue start"), (5, "cta merge done"), (7, "cluster sync 1"),
+                   (9, "outputs written"), (6, "epilogue done")]:
         v = rel[:, k][rel[:, k] >= 0] / 1e3
         if v.size:
             print(f"   {lab:20s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f} us")
