@@ -36,6 +36,12 @@ extern "C" int delta_trace_read(void* host, size_t bytes) {  // copies then clea
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     return (int)e;
 }
+extern "C" int delta_trace_read_smid(void* host, size_t bytes) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess)
+        e = cudaMemcpyFromSymbol(host, g_delta_smid, bytes < sizeof(g_delta_smid) ? bytes : sizeof(g_delta_smid));
+    return (int)e;
+}
 #endif
 
 namespace delta {
@@ -495,15 +501,25 @@ cudaError_t launch_impl(const AttnParams& p0, const CUtensorMap* tm_kv,
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = p.nsplit;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[3];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = p.nsplit;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+    if (p.cluster_policy) {
+        attr[na].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+        attr[na].val.clusterSchedulingPolicyPreference = (cudaClusterSchedulingPolicy)p.cluster_policy;
+        ++na;
+    }
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 2 : 1;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, *tm_kv, p);
 }
 

@@ -267,7 +267,7 @@ struct delta_ctx {
     // tcgen05 kernel (attn_umma.cu): correct, but one tcgen05.mma of a 16-token tile costs ~48
     // cycles to issue (tools/umma_test.cu), so 10 per tile lose to the mma.sync kernel here;
     // kept selectable (DELTA_TUNE umma=1) and parity-tested.
-    int tune_prewait = 1, tune_early = 1, tune_umma = 0;
+    int tune_prewait = 1, tune_early = 1, tune_umma = 0, tune_policy = 0;
     // sequence sharding
     int world = 1, rank = 0, page_lo = 0, page_hi = 0x7fffffff;
     ncclComm_t comm = nullptr;  // null with world > 1: the caller exchanges (delta_shard_* calls)
@@ -392,6 +392,7 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
     // this order; eager calls may follow other work on the stream.
     p.prewait = (in_step && h->tune_prewait) ? 1 : 0;
     p.early_trigger = h->tune_early;
+    p.cluster_policy = h->tune_policy;
     if (h->last_kind == delta_ctx::kLastNone) p.prewait = 0;
     if (h->last_layer == layer && (h->last_kind == delta_ctx::kLastAppend || h->last_kind == delta_ctx::kLastAttn))
         p.prewait = 0;
@@ -630,6 +631,7 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
         if (const char* w = std::strstr(t, "snsplit=")) h->tune_snsplit = std::atoi(w + 8);
         if (const char* w = std::strstr(t, "early=")) h->tune_early = std::atoi(w + 6);
         if (const char* w = std::strstr(t, "umma=")) h->tune_umma = std::atoi(w + 5);
+        if (const char* w = std::strstr(t, "policy=")) h->tune_policy = std::atoi(w + 7);
     }
     h->step.assign(cfg->num_layers, 0);
     h->dec_step.assign(cfg->num_layers, -1);

@@ -35,6 +35,7 @@ struct AttnParams {
     int deep;           // 1: one CTA per SM with the deep TMA ring (few CTAs), 0: shallow ring
     int prewait;        // 1: start geometry + KV stream before griddepcontrol.wait (see attn_tc.cu)
     int early_trigger;  // 1: launch_dependents right after the wait (else after the main loop)
+    int cluster_policy; // cudaClusterSchedulingPolicy for the split-K cluster (0 = default)
     float scale;        // softmax scale (natural units)
     float scale_log2;   // scale * log2(e)
     const void* q;      // [batch][m][d]

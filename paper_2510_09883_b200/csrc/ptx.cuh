@@ -10,6 +10,7 @@
 // Phase timestamps (%globaltimer, ns) per (layer, CTA) for latency analysis; trace builds
 // only (`make trace`), never the product library.  Uses `p.layer` of the enclosing kernel.
 static __device__ unsigned long long g_delta_trace[64 * 512 * 12];
+static __device__ unsigned int g_delta_smid[64 * 512];  // SM of each traced CTA
 #define DTRACE(slot)                                                                          \
     do {                                                                                      \
         unsigned long long t_;                                                                \
@@ -17,6 +18,11 @@ static __device__ unsigned long long g_delta_trace[64 * 512 * 12];
         const unsigned cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
         if (cta_ < 512 && (p.layer + DTRACE_LAYER_OFF) < 64)                                   \
             g_delta_trace[((p.layer + DTRACE_LAYER_OFF) * 512 + cta_) * 12 + (slot)] = t_;      \
+        if ((slot) == 0 && cta_ < 512 && (p.layer + DTRACE_LAYER_OFF) < 64) {                 \
+            unsigned sm_;                                                                     \
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));                                  \
+            g_delta_smid[(p.layer + DTRACE_LAYER_OFF) * 512 + cta_] = sm_;                    \
+        }                                                                                     \
     } while (0)
 #ifndef DTRACE_LAYER_OFF
 #define DTRACE_LAYER_OFF 0

@@ -32,6 +32,18 @@ def read():
     return a.copy()
 
 
+def smid_report(layer, ncta):
+    """How the CTAs of the last traced launch of `layer` were placed: CTAs per SM."""
+    sm = np.zeros(64 * 512, np.uint32)
+    if not hasattr(lib, "delta_trace_read_smid"):
+        return
+    assert lib.delta_trace_read_smid(sm.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(sm.nbytes)) == 0
+    ids = sm.reshape(64, 512)[layer, :ncta]
+    per = np.bincount(ids, minlength=148)
+    print(f"   placement L{layer}: {int((per > 0).sum())} SMs used, {int((per == 2).sum())} with 2 CTAs, "
+          f"{int((per > 2).sum())} with >2")
+
+
 def per_cluster(tr3, nsplit=16, slot=3):
     """loop-done spread per cluster (head) of one layer's trace: is the skew per GPC or per CTA?"""
     t = tr3.reshape(-1, 12)
@@ -109,6 +121,7 @@ def main():
                 s.synchronize()
                 tr_ = read()
                 report(f"{name} rep {rep}", tr_)
+                smid_report(0 if name.startswith("FULL") else 3, 128)
                 if os.environ.get("PROBE_CLUSTERS"):
                     per_cluster(tr_[0] if name.startswith("FULL") else tr_[3])
             if os.environ.get("PROBE_TILES"):
