@@ -235,8 +235,12 @@ class DeltaStack:
         pool_bytes, ws_bytes = query_sizes(cfg)
         dt = torch.bfloat16 if cfg.kv_dtype == DELTA_BF16 else torch.float32
         shape = (cfg.num_layers, cfg.phys_pages, cfg.num_kv_heads, 2, cfg.page_size, cfg.head_dim)
-        kv_pool = torch.zeros(shape, dtype=dt, device=device)
-        assert kv_pool.numel() * kv_pool.element_size() == pool_bytes
+        # the caching allocator guarantees 512-byte alignment only: over-allocate and align the
+        # pool to the 1024 bytes its TMA descriptor (128-byte swizzle) needs
+        raw = torch.zeros(pool_bytes + 1024, dtype=torch.uint8, device=device)
+        off = (-raw.data_ptr()) % 1024
+        kv_pool = raw[off: off + pool_bytes].view(dt).view(shape)
+        assert kv_pool.data_ptr() % 1024 == 0
         ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=device)
         bt = block_table.to(device=device, dtype=torch.int32).contiguous()
         return cls(cfg, kv_pool, bt, ws)

@@ -69,8 +69,8 @@ struct TcCfg {
     static constexpr int kSmem = 1024 + kRing + ClusterStage<D>::kBytes + 2 * NSTAGE * 8 + kRowTok * 4 + 16;
 };
 
-template <int D, bool TOKEN_PLAN, int NSTAGE, int NH, int NG>
-__global__ void __launch_bounds__(cta_threads<NG>(), NH == 1 ? 2 : 1)  // two CTAs per SM (cluster residency)
+template <int D, bool TOKEN_PLAN, int NSTAGE, int NH, int NG, bool CL>
+__global__ void __launch_bounds__(cta_threads<NG>(), (NH == 1 && CL) ? 2 : 1)  // cluster: two CTAs per SM
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     static_assert(NSTAGE % NG == 0, "ring slots must map to fixed consumer groups");
     constexpr int NCW = NT * NG;  // consumer warps; warp NCW is the producer
@@ -93,14 +93,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
             mbar_init(&full[i], TOKEN_PLAN ? 32 : 1);
             mbar_init(&empty[i], NT);
         }
-        cluster_stage_init<D>(cstage, p.gs);
+        if (CL) cluster_stage_init<D>(cstage, p.gs);
         fence_mbar_init();
     }
     if (!TOKEN_PLAN && warp == NCW && lane == 0) {
         tma_prefetch_desc(&tm_kv);
     }
     __syncthreads();
-    cluster_arrive_relaxed();  // peers may push into cstage once they pass the matching wait
+    if (CL) cluster_arrive_relaxed();  // peers may push into cstage once they pass the matching wait
     if (tid == 0) DTRACE(0);
     // Programmatic dependent launch: without `prewait` everything waits for the previous
     // kernel here.  With `prewait` (the host knows the previous kernel of this handle wrote
@@ -151,6 +151,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     constexpr int OSR = 8 * NH;  // O rows kept per warp (the group's heads, gs <= 8 * NH)
     static_assert((2 * NCW * 16 + NCW * OSR * os_stride<D>()) * 4 <= TcCfg<D, NSTAGE>::kRing,
                   "epilogue state must fit in the K ring");
+    // global-merge scratch (weights, L_c, merged M/L) in the ring past the warp states
+    constexpr int kMergeScratch = 2 * NCW * 16 + NCW * OSR * os_stride<D>();
+    // (n outputs of the slice x ns partials, float4 O + float2 (M, L) each; n * ns <= total + ns)
+    static_assert(CL || (kMergeScratch + 6 * (kMaxGs * D / 4 + kMaxSplitG) + 64) * 4 <= TcCfg<D, NSTAGE>::kRing,
+                  "merge scratch must fit in the ring");
 
     if (warp == NCW) {
         // ============================================================ producer
@@ -477,22 +482,24 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     __syncthreads();  // producer joins: warp states complete
     if (!p.early_trigger) pdl_launch_dependents();
     if (tid == 0) DTRACE(4);
-    cluster_epilogue<D, NCW, OSR>(p, ms, ls, os, cstage, b, h, stale, cap_err, s);
+    if (CL) cluster_epilogue<D, NCW, OSR>(p, ms, ls, os, cstage, b, h, stale, cap_err, s);
+    else global_epilogue<D, NCW, OSR>(p, ms, ls, os, reinterpret_cast<float*>(ring) + kMergeScratch, b, h, split,
+                                       stale, cap_err, s);
     if (tid == 0) DTRACE(6);
 }
 
-template <int D, bool TOKEN_PLAN, int NST, int NH, int NG>
+template <int D, bool TOKEN_PLAN, int NST, int NH, int NG, bool CL = true>
 cudaError_t launch_impl(const AttnParams& p0, const CUtensorMap* tm_kv,
                         cudaStream_t st, bool pdl) {
-    auto kern = attn_tc_kernel<D, TOKEN_PLAN, NST, NH, NG>;
+    auto kern = attn_tc_kernel<D, TOKEN_PLAN, NST, NH, NG, CL>;
     constexpr int kThreads = cta_threads<NG>();
     constexpr int smem = TcCfg<D, NST>::kSmem;
     static int max_cluster = 0;  // largest feasible cluster for this instantiation
     if (max_cluster == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e == cudaSuccess && CL) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
-        max_cluster = cluster_limit((const void*)kern, kThreads, smem);
+        max_cluster = CL ? cluster_limit((const void*)kern, kThreads, smem) : kMaxSplitG;
     }
     AttnParams p = p0;
     p.nsplit = std::min(p.nsplit, max_cluster);
@@ -503,12 +510,14 @@ cudaError_t launch_impl(const AttnParams& p0, const CUtensorMap* tm_kv,
     cfg.stream = st;
     cudaLaunchAttribute attr[3];
     int na = 0;
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = p.nsplit;
-    attr[na].val.clusterDim.y = 1;
-    attr[na].val.clusterDim.z = 1;
-    ++na;
-    if (p.cluster_policy) {
+    if (CL) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = p.nsplit;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (CL && p.cluster_policy) {
         attr[na].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
         attr[na].val.clusterSchedulingPolicyPreference = (cudaClusterSchedulingPolicy)p.cluster_policy;
         ++na;
@@ -523,9 +532,16 @@ cudaError_t launch_impl(const AttnParams& p0, const CUtensorMap* tm_kv,
     return cudaLaunchKernelEx(&cfg, kern, *tm_kv, p);
 }
 
+// Global-merge variant: one CTA per SM, nine consumer warps (a sparse layer's ~8 tiles per CTA
+// in one round), six ring stages of three tiles (144 KiB in flight per SM).
+constexpr int kGStage = 6, kGGroups = 3;
+
 template <int D, bool TOKEN_PLAN>
 cudaError_t launch_stages(const AttnParams& p, const CUtensorMap* tm_kv, cudaStream_t st,
                           bool pdl) {
+    if (p.gmerge)
+        return p.gs <= 8 ? launch_impl<D, TOKEN_PLAN, kGStage, 1, kGGroups, false>(p, tm_kv, st, pdl)
+                         : launch_impl<D, TOKEN_PLAN, kGStage, 2, kGGroups, false>(p, tm_kv, st, pdl);
     if (p.gs <= 8)
         return p.deep ? launch_impl<D, TOKEN_PLAN, kDeep, 1, 2>(p, tm_kv, st, pdl)
                       : launch_impl<D, TOKEN_PLAN, kShallow, 1, 2>(p, tm_kv, st, pdl);
@@ -538,7 +554,7 @@ cudaError_t launch_stages(const AttnParams& p, const CUtensorMap* tm_kv, cudaStr
 #ifdef DELTA_TRACE
 // trace builds: max co-resident clusters of the real kernel for a cluster size
 extern "C" int delta_debug_cluster_occupancy(int deep, int cs) {
-    auto kern = deep ? attn_tc_kernel<128, false, kDeep, 1, 2> : attn_tc_kernel<128, false, kShallow, 1, 2>;
+    auto kern = deep ? attn_tc_kernel<128, false, kDeep, 1, 2, true> : attn_tc_kernel<128, false, kShallow, 1, 2, true>;
     const int smem = deep ? TcCfg<128, kDeep>::kSmem : TcCfg<128, kShallow>::kSmem;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -267,4 +267,175 @@ __device__ __forceinline__ void cluster_epilogue(const AttnParams& p, const floa
     }
 }
 
+// Split-K epilogue without a cluster (AttnParams::gmerge), called by every thread of the CTA
+// after the warp states are complete in shared memory:
+//  1. fold the NW warp states in fixed warp order into this CTA's (M_c, L_c, O_c) (as in
+//     cluster_epilogue step 1); with one split the CTA normalises and writes the outputs itself;
+//  2. otherwise store the partial to its slot in p.gpart and draw a ticket from the (b, h, ns)
+//     counter with one acq_rel atomic (the barrier before it puts every thread's stores in the
+//     release); wait until the ns tickets of this launch are drawn (every CTA of a launch is
+//     resident or will be: the grid is at most one wave, and nothing it waits on waits on it);
+//  3. like the cluster owners, CTA `split` merges its slice of the gs x D outputs from all ns
+//     partials in ascending split order (deterministic): one round of loads into shared memory,
+//     then M = max_c M_c, w_c = exp2(M_c - M), L = sum_c w_c L_c, O = sum_c w_c O_c / L.
+//  Split 0 does the once-per-(b, h) duties (error flags, fused-append counter).
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int32_t* a, int v) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned long long atom_add_acq_rel_gpu_u64(unsigned long long* a, unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], %2;" : "=l"(old) : "l"(a), "l"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t* a) {
+    int v;
+    asm volatile("ld.acquire.gpu.s32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int32_t* a, int v) {
+    asm volatile("st.release.gpu.s32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+
+template <int D, int NW, int OSROWS>
+__device__ __forceinline__ void global_epilogue(const AttnParams& p, const float* ms, const float* ls,
+                                                const float* os, float* scratch, int b, int h, int split,
+                                                bool stale, bool cap_err, int s_post) {
+    const int tid = threadIdx.x, nthreads = blockDim.x;
+    const int gs = p.gs, ns = p.nsplit;
+    constexpr int C4 = D / 4, OS = os_stride<D>();
+    const int total = gs * C4;
+    const size_t rec = (size_t)gpart_floats(D);
+    float* my = p.gpart + (((size_t)b * p.g + h) * ns + split) * rec;
+    const bool shard = p.shard_world > 1;
+    bool bad = false;
+    auto emit = [&](int row, int c4, float M, float L, float4 v) {
+        const float inv = (L > 0.f) ? __frcp_rn(L) : 0.f;
+        float4 o = make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv);
+        if (stale) {
+            const float qn = __int_as_float(0x7fc00000);  // NaN: stale plan must be loud
+            o = make_float4(qn, qn, qn, qn);
+        } else if (!(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w))) {
+            bad = true;
+        }
+        const int j = h * gs + row;
+        reinterpret_cast<float4*>((shard ? p.part_o : p.out) + ((size_t)b * p.m + j) * D)[c4] = o;
+        if (c4 == 0) {
+            const float lse = (L > 0.f) ? (M + log2f(L)) * kLn2 : -INFINITY;
+            if (shard) {
+                p.part_lse[(size_t)b * p.m + j] = lse;
+            } else {
+                if (p.lse_out) p.lse_out[(size_t)b * p.m + j] = lse;
+                if (p.role == kRoleSelect) p.lse_buf[(size_t)b * p.m + j] = lse;
+            }
+        }
+    };
+    // 1. this CTA's state
+    for (int idx = tid; idx < total; idx += nthreads) {
+        const int row = idx / C4, c4 = idx - row * C4;
+        float mw[NW];
+        float4 v[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            mw[w] = ms[w * 16 + row];
+            v[w] = reinterpret_cast<const float4*>(os + (w * OSROWS + row) * OS)[c4];
+        }
+        float M = mw[0];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) M = fmaxf(M, mw[w]);
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        float L = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const float f = (M == -INFINITY || mw[w] == -INFINITY) ? 0.f : exp2f(mw[w] - M);
+            o.x += f * v[w].x; o.y += f * v[w].y; o.z += f * v[w].z; o.w += f * v[w].w;
+            L += ls[w * 16 + row] * f;
+        }
+        if (ns == 1) {
+            emit(row, c4, M, L, o);
+        } else {
+            reinterpret_cast<float4*>(my + (size_t)row * D)[c4] = o;
+            if (c4 == 0) reinterpret_cast<float2*>(my + kMaxGs * D)[row] = make_float2(M, L);
+        }
+    }
+    if (ns > 1) {
+        // 2. arrive (ticket on the (b, h, ns) 64-bit counter: launches with this split count
+        //    always add exactly ns, so the counter is a multiple of ns between launches) and
+        //    wait until all ns tickets of this launch are drawn
+        __syncthreads();
+        if (tid == 0) DTRACE(5);
+        if (tid == 0) {
+            unsigned long long* cnt = p.gcnt + ((size_t)b * p.g + h) * kMaxSplitG + (ns - 1);
+            const unsigned long long old = atom_add_acq_rel_gpu_u64(cnt, 1ull);
+            const unsigned long long target = old - old % (unsigned long long)ns + (unsigned long long)ns;
+            if (old + 1 != target) {
+                while (ld_acquire_gpu_u64(cnt) < target) {
+                }
+            }
+            DTRACE(7);
+        }
+        __syncthreads();
+        // 3. merge this CTA's slice [lo, lo + n) of the outputs: one round of loads into shared
+        //    memory, then one warp per output, split c on lane c (and c - 32), fixed xor trees
+        const int per = (total + ns - 1) / ns, lo = split * per, n = max(0, min(total, lo + per) - lo);
+        const float* base = p.gpart + ((size_t)b * p.g + h) * ns * rec;
+        float4* sx = reinterpret_cast<float4*>(scratch);          // [n][ns] partial O
+        float2* sml = reinterpret_cast<float2*>(sx + per * ns);   // [n][ns] (M_c, L_c) of the row
+        for (int i = tid; i < n * ns; i += nthreads) {
+            const int k = i / ns, c = i - k * ns;
+            const int idx = lo + k, row = idx / C4, c4 = idx - row * C4;
+            sx[i] = __ldcg(reinterpret_cast<const float4*>(base + c * rec + (size_t)row * D) + c4);
+            sml[i] = __ldcg(reinterpret_cast<const float2*>(base + c * rec + kMaxGs * D) + row);
+        }
+        __syncthreads();
+        if (tid == 0) DTRACE(9);
+        const int lane = tid & 31, warp = tid >> 5, nwarps = nthreads >> 5;
+        for (int k = warp; k < n; k += nwarps) {
+            const int idx = lo + k, row = idx / C4, c4 = idx - row * C4;
+            float2 ml[2];
+            float4 x[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int c = lane + 32 * j;
+                ml[j] = c < ns ? sml[k * ns + c] : make_float2(-INFINITY, 0.f);
+                x[j] = c < ns ? sx[k * ns + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            float M = fmaxf(ml[0].x, ml[1].x);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+            float L = 0.f;
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const float f = (M == -INFINITY || ml[j].x == -INFINITY) ? 0.f : exp2f(ml[j].x - M);
+                L += f * ml[j].y;
+                o.x += f * x[j].x; o.y += f * x[j].y; o.z += f * x[j].z; o.w += f * x[j].w;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                L += __shfl_xor_sync(0xffffffffu, L, off);
+                o.x += __shfl_xor_sync(0xffffffffu, o.x, off);
+                o.y += __shfl_xor_sync(0xffffffffu, o.y, off);
+                o.z += __shfl_xor_sync(0xffffffffu, o.z, off);
+                o.w += __shfl_xor_sync(0xffffffffu, o.w, off);
+            }
+            if (lane == 0) emit(row, c4, M, L, o);
+        }
+    }
+    if (bad) set_err(p.err, kDevNumeric);
+    if (split == 0 && tid == 0) {
+        if (stale) set_err(p.err, kDevUsage);
+        if (cap_err) set_err(p.err, kDevCapacity);
+        if (s_post <= 0) set_err(p.err, kDevUsage);  // attention over an empty cache
+        // after the wait: every CTA of (b, h) has read the length counter
+        if (p.fuse_append && !cap_err) atomicAdd(&p.seq_len[p.layer * p.max_batch + b], 1);
+    }
+}
+
 }  // namespace delta

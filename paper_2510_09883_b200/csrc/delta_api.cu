@@ -29,7 +29,8 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
     size_t seq_len, err, cnt_sel, logits, lse_buf, keys, plan_idx, plan_phys, plan_count, plan_stamp, plan_lo, plan_hi,
-        shard_send, shard_recv, cand_send, cand_recv, stage_q, stage_k, stage_v, stage_out, total;
+        shard_send, shard_recv, cand_send, cand_recv, stage_q, stage_k, stage_v, stage_out, gpart, gcnt, total;
+    int gslots;  // split partial slots of the global-merge kernels
     size_t shard_block, cand_block;  // bytes of one rank's attention partial / candidate block
     int max_units, plan_cap, n_delta, max_pages;
 };
@@ -65,6 +66,17 @@ int nsplit_sparse(const delta_config& c, int batch, int sms, int max_pages, int 
     // 8 splits 383 (a third round per warp).
     const int by_tiles = std::max(1, (plan_tiles(c, plan_cap) + 11) / 12);
     return std::max(1, std::min(full, by_tiles));
+}
+
+// Global-merge kernels (no cluster, one CTA per SM): used when every (sequence, kv head) gets
+// at least one CTA in a single wave, i.e. batch * g <= SMs.  Splits per (b, h) = SMs / (b g)
+// (C1: 18 -> 144 CTAs), for a sparse layer at most one per ~4 plan tiles (nine consumer warps).
+bool use_gmerge(int batch, int g, int sms) { return batch * g <= sms; }
+
+int nsplit_gmerge(int batch, int g, int sms, int items) {
+    int n = sms / std::max(1, batch * g);
+    n = std::max(1, std::min(n, kMaxSplitG));
+    return std::min(n, std::max(1, items));
 }
 
 // The deep-ring variant (one CTA per SM) is kept for experiments (DELTA_TUNE deep=1).
@@ -164,6 +176,9 @@ Layout layout(const delta_config& c, int sms) {
     L.stage_k = take((size_t)c.num_layers * c.max_batch * g * D * e);
     L.stage_v = take((size_t)c.num_layers * c.max_batch * g * D * e);
     L.stage_out = take((size_t)c.num_layers * c.max_batch * m * D * 4);
+    L.gslots = std::max(sms, 1) * 2;  // batch * g * nsplit <= sms for every gmerge launch
+    L.gpart = take((size_t)L.gslots * gpart_floats(D) * 4);
+    L.gcnt = take((size_t)c.max_batch * g * kMaxSplitG * 8);  // ticket counter per (b, h, split count)
     L.total = off;
     return L;
 }
@@ -268,6 +283,7 @@ struct delta_ctx {
     // cycles to issue (tools/umma_test.cu), so 10 per tile lose to the mma.sync kernel here;
     // kept selectable (DELTA_TUNE umma=1) and parity-tested.
     int tune_prewait = 1, tune_early = 1, tune_umma = 0, tune_policy = 0;
+    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1;
     // sequence sharding
     int world = 1, rank = 0, page_lo = 0, page_hi = 0x7fffffff;
     ncclComm_t comm = nullptr;  // null with world > 1: the caller exchanges (delta_shard_* calls)
@@ -327,8 +343,19 @@ AttnParams attn_params(delta_ctx* h, int layer, int batch) {
             p.plan_hi = h->at<int32_t>(h->L.plan_hi) + (size_t)sl * c.max_batch;
         }
     }
-    if (h->tune_nsplit > 0) p.nsplit = std::min(h->tune_nsplit, kMaxSplit);
-    if (h->tune_snsplit > 0 && p.role == kRoleSparse) p.nsplit = std::min(h->tune_snsplit, kMaxSplit);
+    // (the tcgen05 and fp32 kernels keep the cluster merge)
+    //  tune_gmerge: 0 never, 1 full-cache layers (FULL / SELECT), 2 every role
+    const bool gm_role = h->tune_gmerge == 2 || (h->tune_gmerge == 1 && p.role != kRoleSparse);
+    p.gmerge = (gm_role && h->use_tc && !h->tune_umma && use_gmerge(batch, c.num_kv_heads, h->sms)) ? 1 : 0;
+    if (p.gmerge) {
+        const int items = p.role == kRoleSparse ? (plan_tiles(c, h->L.plan_cap) + 3) / 4 : h->L.max_pages;
+        p.nsplit = nsplit_gmerge(batch, c.num_kv_heads, h->sms, items);
+        p.gpart = h->at<float>(h->L.gpart);
+        p.gcnt = h->at<unsigned long long>(h->L.gcnt);
+    }
+    const int cap = p.gmerge ? std::min(kMaxSplitG, h->L.gslots / std::max(1, batch * c.num_kv_heads)) : kMaxSplit;
+    if (h->tune_nsplit > 0) p.nsplit = std::min(h->tune_nsplit, cap);
+    if (h->tune_snsplit > 0 && p.role == kRoleSparse) p.nsplit = std::min(h->tune_snsplit, cap);
     p.deep = deep_ring(batch, c.num_kv_heads, p.nsplit, h->sms) ? 1 : 0;
     if (h->tune_deep >= 0) p.deep = h->tune_deep;
     return p;
@@ -422,6 +449,8 @@ delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_ov
     const int sl = h->slot[layer];
     p.m = c.num_q_heads; p.g = c.num_kv_heads; p.layer = layer; p.batch = batch;
     p.nchunk = std::max(1, std::min((h->L.max_units + 15) / 16, (2 * h->sms + batch - 1) / batch));
+    p.late_trigger = h->tune_seltrig;
+    p.hist_mode = h->tune_selhist;
     p.sel_block = c.select_block; p.n_sink = c.n_sink; p.n_window = c.n_window;
     p.k_units = c.budget_k / c.select_block;
     p.max_batch = c.max_batch; p.max_seq = c.max_seq_len; p.max_units = h->L.max_units; p.plan_cap = h->L.plan_cap;
@@ -632,6 +661,9 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
         if (const char* w = std::strstr(t, "early=")) h->tune_early = std::atoi(w + 6);
         if (const char* w = std::strstr(t, "umma=")) h->tune_umma = std::atoi(w + 5);
         if (const char* w = std::strstr(t, "policy=")) h->tune_policy = std::atoi(w + 7);
+        if (const char* w = std::strstr(t, "seltrig=")) h->tune_seltrig = std::atoi(w + 8);
+        if (const char* w = std::strstr(t, "gmerge=")) h->tune_gmerge = std::atoi(w + 7);
+        if (const char* w = std::strstr(t, "selhist=")) h->tune_selhist = std::atoi(w + 8);
     }
     h->step.assign(cfg->num_layers, 0);
     h->dec_step.assign(cfg->num_layers, -1);

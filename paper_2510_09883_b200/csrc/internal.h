@@ -13,6 +13,9 @@ enum DevErr : int { kDevOk = 0, kDevUsage = 2, kDevNumeric = 3, kDevCapacity = 4
 constexpr int kPage = 16;        // P
 constexpr int kMaxGs = 16;       // query heads per KV group handled by one MMA row tile
 constexpr int kMaxSplit = 16;    // split-K CTAs per (sequence, kv head) = one thread-block cluster
+constexpr int kMaxSplitG = 64;   // split-K CTAs per (sequence, kv head) with the global merge
+// Floats of one split's partial in the global-merge buffer: O rows [kMaxGs][d] then (M, L) pairs.
+__host__ __device__ constexpr int gpart_floats(int d) { return kMaxGs * d + 2 * kMaxGs; }
 
 // Row (of d elements) holding slot `slot` of the K head-page of (layer_page, head h), where
 // layer_page = layer * num_phys + physical page; the matching V row is kv_row(...) + kPage.
@@ -36,6 +39,10 @@ struct AttnParams {
     int prewait;        // 1: start geometry + KV stream before griddepcontrol.wait (see attn_tc.cu)
     int early_trigger;  // 1: launch_dependents right after the wait (else after the main loop)
     int cluster_policy; // cudaClusterSchedulingPolicy for the split-K cluster (0 = default)
+    int gmerge;         // 1: no cluster; one CTA per SM; splits merged through global memory by
+                        //    the last-arriving CTA of each (sequence, kv head) (combine.cuh)
+    float* gpart;       // gmerge: [batch][g][nsplit][gpart_floats(d)] split partials
+    unsigned long long* gcnt;  // gmerge: [max_batch][g][kMaxSplitG] ticket counters, by split count
     float scale;        // softmax scale (natural units)
     float scale_log2;   // scale * log2(e)
     const void* q;      // [batch][m][d]
@@ -88,6 +95,8 @@ struct SelectParams {
     // scattered from all ranks' candidates; also writes this rank's plan range lo/hi)
     int shard_mode, page_lo, page_hi;
     uint2* cand_out;            // mode 1: [batch][k_units] (order-preserving key bits, unit)
+    int late_trigger;           // 1: launch dependents after the plan is written (else at entry)
+    int hist_mode;              // radix histogram: 0 per-warp private, 1 warp-aggregated shared
     int32_t* plan_lo;           // [max_batch]
     int32_t* plan_hi;
 };

@@ -57,12 +57,36 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scratch, int* total) 
     return warp_excl + x - v;
 }
 
+// Exclusive block-wide prefix sum with ONE barrier: warp totals go to scratch[0..kSelWarps),
+// then every warp sums the totals below it itself.  `scratch` must not be reused before
+// the next barrier.
+__device__ __forceinline__ int block_excl_scan1(int v, int* scratch, int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) scratch[warp] = x;
+    __syncthreads();
+    const int t = lane < kSelWarps ? scratch[lane] : 0;
+    int below = lane < warp ? t : 0, all = t;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        below += __shfl_xor_sync(0xffffffffu, below, off);
+        all += __shfl_xor_sync(0xffffffffu, all, off);
+    }
+    *total = all;
+    return below + x - v;
+}
+
 // max_j (a_j(t) - LSE_j) over the heads j this lane owns: lane pair (hh = 0, 1) splits the m
 // heads of token t; lane hh owns the 16-byte head groups q = hh, hh+2, ... (m % 4 == 0; the
 // row is 16-byte aligned because the logits are [s][m] fp32).  `lse4` holds this lane's LSE
 // groups in registers.  Max is exact, so the split and the order do not change the result.
 struct LseLane {
-    float4 v[8];  // q = hh + 2i, i < 8 (m <= 64); larger m falls back to global loads
+    float4 v[4];  // q = hh + 2i, i < 4 (m <= 32); larger m falls back to global loads
 };
 
 __device__ __forceinline__ float head_max(const float* __restrict__ row, const LseLane& ls,
@@ -71,14 +95,14 @@ __device__ __forceinline__ float head_max(const float* __restrict__ row, const L
     if ((m & 3) == 0) {
         const float4* r4 = reinterpret_cast<const float4*>(row);
         const int n4 = m >> 2;
-        float4 v[8];
+        float4 v[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 4; ++i) {
             const int q = hh + 2 * i;
             v[i] = q < n4 ? r4[q] : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 4; ++i) {
             const int q = hh + 2 * i;
             if (q < n4) {
                 const float4 l = ls.v[i];
@@ -86,7 +110,7 @@ __device__ __forceinline__ float head_max(const float* __restrict__ row, const L
             }
         }
         const float4* l4 = reinterpret_cast<const float4*>(lse_g);
-        for (int q = hh + 16; q < n4; q += 2) {
+        for (int q = hh + 8; q < n4; q += 2) {
             const float4 w = r4[q], l = l4[q];
             mx = fmaxf(mx, fmaxf(fmaxf(w.x - l.x, w.y - l.y), fmaxf(w.z - l.z, w.w - l.w)));
         }
@@ -97,18 +121,169 @@ __device__ __forceinline__ float head_max(const float* __restrict__ row, const L
     return mx;
 }
 
-__global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams p) {
+// Register-resident top-k (phase B) for n_units <= kSelThreads * IPT: thread t holds units
+// [t*IPT, t*IPT + IPT) — keys, candidate flags — loaded with one round of independent loads;
+// the radix passes and the compaction then run on-chip (2 barriers per pass).  Returns the
+// plan length.  Instantiated for IPT = 4 / 8 / 16 so no predicated-off slots are executed.
+template <int IPT>
+__device__ __forceinline__ int topk_regs(const SelectParams& p, int n_units, int sink_hi, int win_lo, int block,
+                                      const float* __restrict__ src, const int32_t* __restrict__ bt,
+                                      int32_t* plan, int32_t* plan_phys, uint32_t* sm_keys, int* hist2,
+                                      int* scratch, uint32_t& s_and, uint32_t& s_or, int& s_bin, int& s_rem,
+                                      int& s_cnt) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    auto forced = [&](int u) { return u < sink_hi || u >= win_lo; };
+    auto phys_of = [&](int u) -> int32_t { return block == 1 ? bt[u / kPage] * kPage + (u % kPage) : bt[u]; };
+    // ---- register-resident path: thread t holds units [t*ipt, t*ipt + ipt) — keys,
+    // candidate flags and physical locations — loaded with one round of independent loads;
+    // the radix passes and the compaction then run on-chip (2 barriers per pass).
+    const int ipt = IPT;
+    const int u0 = tid * ipt;
+    uint32_t key[IPT];
+    int32_t* s_phys = reinterpret_cast<int32_t*>(sm_keys);  // unused key cache: >= n_units slots
+    uint32_t cand = 0, live = 0;
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        const int u = u0 + i;
+        const bool in = i < ipt && u < n_units;
+        const float f = in ? __ldcg(src + u) : 0.f;
+        if (in) s_phys[u] = phys_of(u);
+        key[i] = key_bits(f);
+        bad |= in && isnan(f);
+        if (in) live |= 1u << i;
+        if (in && !forced(u)) cand |= 1u << i;
+    }
+    if (bad) set_err(p.err, kDevNumeric);
+    // leading bits every candidate shares (block AND / OR): the radix passes start at the
+    // first byte where the candidates differ
+    uint32_t kand = 0xffffffffu, kor = 0u;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i)
+        if (cand & (1u << i)) {
+            kand &= key[i];
+            kor |= key[i];
+        }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        kand &= __shfl_xor_sync(0xffffffffu, kand, off);
+        kor |= __shfl_xor_sync(0xffffffffu, kor, off);
+    }
+    if (lane == 0) {
+        atomicAnd(&s_and, kand);
+        atomicOr(&s_or, kor);
+    }
+    __syncthreads();
+    if (tid == 0) DTRACE(6);
+    const uint32_t same = ~(s_and ^ s_or);
+    int first_pass = 0;
+    while (first_pass < 3 && ((same >> (24 - 8 * first_pass)) & 0xFFu) == 0xFFu) ++first_pass;
+    uint32_t maskbits = first_pass == 0 ? 0u : ~((1u << (32 - 8 * first_pass)) - 1u);
+    uint32_t prefix = s_and & maskbits;
+    int remaining = p.k_units, bin_cnt = 0;
+    // One barrier per pass: every warp walks the histogram itself (same result in every warp).
+    // Four buffers: pass p fills buffer p % 4 (zeroed during pass p - 2, before that pass's
+    // barrier) and zeroes buffer (p + 2) % 4, last read in pass p - 2's walk, which every warp
+    // finished before it could arrive at pass p - 1's barrier.
+    for (int pass = p.k_units > 0 ? first_pass : 4; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        int* h = hist2 + (pass & 3) * 256;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i)
+            if ((cand & (1u << i)) && (key[i] & maskbits) == prefix) atomicAdd(&h[(key[i] >> shift) & 255u], 1);
+        if (tid < 256) hist2[((pass + 2) & 3) * 256 + tid] = 0;
+        __syncthreads();
+        // walk the 256 bins in descending order: lane owns bins 255 - 8 lane - k
+        int c[8], sum = 0;
+        {
+            const int4* h4 = reinterpret_cast<const int4*>(h + 248 - 8 * lane);
+            const int4 x = h4[0], y = h4[1];  // bins 248-8l .. 255-8l ascending
+            c[0] = y.w; c[1] = y.z; c[2] = y.y; c[3] = y.x; c[4] = x.w; c[5] = x.z; c[6] = x.y; c[7] = x.x;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sum += c[k];
+        int incl = sum;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+        }
+        int excl = incl - sum, bin = 0, rem = 0, cnt = 0;
+        const bool mine = excl < remaining && incl >= remaining;
+        if (mine) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (excl + c[k] >= remaining) {
+                    bin = 255 - (lane * 8 + k);
+                    rem = remaining - excl;
+                    cnt = c[k];
+                    break;
+                }
+                excl += c[k];
+            }
+        }
+        const int src_lane = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        bin = __shfl_sync(0xffffffffu, bin, src_lane);
+        rem = __shfl_sync(0xffffffffu, rem, src_lane);
+        cnt = __shfl_sync(0xffffffffu, cnt, src_lane);
+        prefix |= (uint32_t)bin << shift;
+        maskbits |= 0xFFu << shift;
+        remaining = rem;
+        bin_cnt = cnt;
+        if (tid == 0) DTRACE(7 + pass);
+    }
+    if (tid == 0) DTRACE(4);
+    // selection: forced, key > T, and the lowest-index `remaining` of the keys == T
+    // (all of them when no tie straddles the boundary: one scan instead of two)
+    const uint32_t T = prefix;
+    uint32_t fl_sel = live & ~cand, fl_eq = 0;
+    if (p.k_units == 0) cand = 0;  // forced units only
+#pragma unroll
+    for (int i = 0; i < IPT; ++i)
+        if (cand & (1u << i)) {
+            if (key[i] > T) fl_sel |= 1u << i;
+            else if (key[i] == T) fl_eq |= 1u << i;
+        }
+    int tot;
+    if (remaining < bin_cnt) {  // ties at T: rank the equal keys by index
+        int eq_rank = block_excl_scan1(__popc(fl_eq), scratch, &tot);
+#pragma unroll
+        for (int i = 0; i < IPT; ++i)
+            if (fl_eq & (1u << i)) {
+                if (eq_rank < remaining) fl_sel |= 1u << i;
+                ++eq_rank;
+            }
+        __syncthreads();  // scratch reuse
+    } else {
+        fl_sel |= fl_eq;
+    }
+    int pos = block_excl_scan1(__popc(fl_sel), scratch + kSelWarps, &tot);
+#pragma unroll
+    for (int i = 0; i < IPT; ++i)
+        if (fl_sel & (1u << i)) {
+            if (pos < p.plan_cap) {
+                plan[pos] = u0 + i;
+                plan_phys[pos] = s_phys[u0 + i];
+            }
+            ++pos;
+        }
+    if (tot > p.plan_cap) set_err(p.err, kDevUsage);
+    return tot;
+}
+
+__global__ void __launch_bounds__(kSelThreads, 2) select_kernel(const SelectParams p) {
     extern __shared__ uint32_t sm_keys[];  // [kSmemUnits] (only when it fits)
-    __shared__ int scratch[kSelWarps + 1];
-    __shared__ int hist[256];
+    __shared__ int scratch[2 * kSelWarps + 1];
+    __shared__ __align__(16) int hist2[4 * 256];  // radix histograms (4 buffers, see topk_regs)
     __shared__ int whist[kSelWarps * 256];
-    __shared__ int s_flag, s_bin, s_rem;
+    __shared__ int s_flag, s_bin, s_rem, s_cnt;
+    __shared__ uint32_t s_and, s_or;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int b = blockIdx.y;
     if (tid == 0) DTRACE(0);
     pdl_wait();
-    pdl_launch_dependents();  // the next kernel's reads of this plan come after its own wait
+    if (!p.late_trigger) pdl_launch_dependents();  // the next kernel's reads of this plan come after its own wait
     if (tid == 0) DTRACE(1);
 
     const int s = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
@@ -124,7 +299,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
         {
             const int hh0 = lane & 1, n4 = p.m >> 2;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < 4; ++i) {
                 const int q = hh0 + 2 * i;
                 lsl.v[i] = ((p.m & 3) == 0 && q < n4) ? reinterpret_cast<const float4*>(lse_g)[q]
                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -187,6 +362,14 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
     const int n_forced = sink_hi + (n_units - win_lo) - max(0, sink_hi - win_lo);
     const int n_cand = n_units - n_forced;
     int count = 0;
+    constexpr int IPT = 8;  // old path: consecutive units per thread, one chunk = 4096 units
+    static_assert(kSelThreads == 512, "two histogram slots per thread");
+    hist2[tid] = 0;
+    hist2[tid + kSelThreads] = 0;
+    if (tid == 0) {
+        s_and = 0xffffffffu;
+        s_or = 0u;
+    }
 
     if (n_cand <= p.k_units) {
         for (int u = tid; u < n_units; u += kSelThreads) {  // R12: budget covers all
@@ -194,6 +377,17 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
             plan_phys[u] = phys_of(u);
         }
         count = n_units;
+    } else if (n_units <= kSelThreads * 16) {
+        const int ipt = (n_units + kSelThreads - 1) / kSelThreads;
+        if (ipt <= 4)
+            count = topk_regs<4>(p, n_units, sink_hi, win_lo, block, src, bt, plan, plan_phys, sm_keys, hist2,
+                                 scratch, s_and, s_or, s_bin, s_rem, s_cnt);
+        else if (ipt <= 8)
+            count = topk_regs<8>(p, n_units, sink_hi, win_lo, block, src, bt, plan, plan_phys, sm_keys, hist2,
+                                 scratch, s_and, s_or, s_bin, s_rem, s_cnt);
+        else
+            count = topk_regs<16>(p, n_units, sink_hi, win_lo, block, src, bt, plan, plan_phys, sm_keys, hist2,
+                                  scratch, s_and, s_or, s_bin, s_rem, s_cnt);
     } else {
         const bool cached = n_units <= kSmemUnits;
         bool bad = false;
@@ -211,34 +405,75 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
         auto K = [&](int u) -> uint32_t { return cached ? sm_keys[u] : key_bits(__ldcg(src + u)); };
 
         if (tid == 0) DTRACE(6);
-        uint32_t prefix = 0, maskbits = 0;
+        // Leading digits every candidate shares (block AND / OR of the candidate keys): those
+        // bits of the k-th key are known, so the radix passes start at the first byte where
+        // the candidates differ (page sums share sign and most exponent bits).
+        uint32_t kand = 0xffffffffu, kor = 0u;
+        for (int u = tid; u < n_units; u += kSelThreads) {
+            if (forced(u)) continue;
+            const uint32_t v = K(u);
+            kand &= v;
+            kor |= v;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            kand &= __shfl_xor_sync(0xffffffffu, kand, off);
+            kor |= __shfl_xor_sync(0xffffffffu, kor, off);
+        }
+        if (lane == 0) {
+            atomicAnd(&s_and, kand);
+            atomicOr(&s_or, kor);
+        }
+        __syncthreads();
+        const uint32_t same = ~(s_and ^ s_or);  // bit set: identical in every candidate
+        int first_pass = 0;
+        while (first_pass < 3 && ((same >> (24 - 8 * first_pass)) & 0xFFu) == 0xFFu) ++first_pass;
+        uint32_t maskbits = first_pass == 0 ? 0u : ~((1u << (32 - 8 * first_pass)) - 1u);
+        uint32_t prefix = s_and & maskbits;
         int remaining = p.k_units;
         if (remaining > 0) {
-            for (int pass = 0; pass < 4; ++pass) {
+            for (int pass = first_pass; pass < 4; ++pass) {
                 const int shift = 24 - 8 * pass;
-                // per-warp private histograms: the keys share their top digits, so a shared
-                // histogram would serialise every warp on the same bins
-                for (int i = tid; i < kSelWarps * 256; i += kSelThreads) whist[i] = 0;
-                __syncthreads();
-                int* myh = whist + warp * 256;
-                for (int u = tid; u < n_units; u += kSelThreads) {
-                    if (forced(u)) continue;
-                    const uint32_t v = K(u);
-                    if ((v & maskbits) == prefix) atomicAdd(&myh[(v >> shift) & 255], 1);
-                }
-                __syncthreads();
-                if (tid < 256) {
-                    int c = 0;
+                int* h = hist2 + (pass & 1) * 256;  // the other buffer was zeroed last pass
+                if (p.hist_mode == 1) {
+                    // warp-aggregated histogram: lanes with the same digit add once
+                    for (int u0 = warp * 32; u0 < n_units; u0 += kSelThreads) {
+                        const int u = u0 + lane;
+                        int bin = -1;
+                        if (u < n_units && !forced(u)) {
+                            const uint32_t v = K(u);
+                            if ((v & maskbits) == prefix) bin = (int)((v >> shift) & 255u);
+                        }
+                        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+                        if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&h[bin], __popc(peers));
+                    }
+                    if (tid < 256) hist2[((pass + 1) & 1) * 256 + tid] = 0;
+                    __syncthreads();
+                } else {
+                    // per-warp private histograms (keys sharing digits do not serialise warps
+                    // on the same bins), then one reduction per bin
+                    for (int i = tid; i < kSelWarps * 256; i += kSelThreads) whist[i] = 0;
+                    __syncthreads();
+                    int* myh = whist + warp * 256;
+                    for (int u = tid; u < n_units; u += kSelThreads) {
+                        if (forced(u)) continue;
+                        const uint32_t v = K(u);
+                        if ((v & maskbits) == prefix) atomicAdd(&myh[(v >> shift) & 255], 1);
+                    }
+                    __syncthreads();
+                    if (tid < 256) {
+                        int c = 0;
 #pragma unroll
-                    for (int w = 0; w < kSelWarps; ++w) c += whist[w * 256 + tid];
-                    hist[tid] = c;
+                        for (int w = 0; w < kSelWarps; ++w) c += whist[w * 256 + tid];
+                        h[tid] = c;
+                    }
+                    __syncthreads();
                 }
-                __syncthreads();
                 if (warp == 0) {  // one warp walks the 256 bins in descending order
                     int c[8], sum = 0;
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        c[k] = hist[255 - (lane * 8 + k)];
+                        c[k] = h[255 - (lane * 8 + k)];
                         sum += c[k];
                     }
                     int incl = sum;
@@ -271,7 +506,6 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
         const uint32_t T = prefix;
         const int need_eq = remaining;  // keys equal to T still to take (lowest index first)
         const bool take_any = p.k_units > 0;
-        constexpr int IPT = 8;          // consecutive units per thread: one chunk = 4096 units
         int carry_eq = 0, carry_pos = 0;
         for (int base = 0; base < n_units; base += kSelThreads * IPT) {
             const int u0 = base + tid * IPT;
@@ -371,6 +605,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
         for (int i = tid; i < p.plan_cap; i += kSelThreads)
             p.idx_out[(size_t)b * p.plan_cap + i] = (i < count) ? plan[i] : -1;
     }
+    if (p.late_trigger) pdl_launch_dependents();
 }
 
 }  // namespace

@@ -32,7 +32,7 @@ def read():
     return a.copy()
 
 
-def smid_report(layer, ncta):
+def smid_report(layer, ncta, tr=None):
     """How the CTAs of the last traced launch of `layer` were placed: CTAs per SM."""
     sm = np.zeros(64 * 512, np.uint32)
     if not hasattr(lib, "delta_trace_read_smid"):
@@ -42,6 +42,14 @@ def smid_report(layer, ncta):
     per = np.bincount(ids, minlength=148)
     print(f"   placement L{layer}: {int((per > 0).sum())} SMs used, {int((per == 2).sum())} with 2 CTAs, "
           f"{int((per > 2).sum())} with >2")
+    if tr is not None:  # loop-done time of CTAs alone on their SM vs sharing it
+        t = tr[layer, :ncta].astype(np.int64)
+        t0 = t[:, 0][t[:, 0] > 0].min()
+        ld = (t[:, 3] - t0) / 1e3
+        shared = per[ids] > 1
+        if shared.any() and (~shared).any():
+            print(f"   loop done: alone med {np.median(ld[~shared]):6.2f} max {ld[~shared].max():6.2f} | "
+                  f"shared med {np.median(ld[shared]):6.2f} max {ld[shared].max():6.2f} us")
 
 
 def per_cluster(tr3, nsplit=16, slot=3):
@@ -121,7 +129,7 @@ def main():
                 s.synchronize()
                 tr_ = read()
                 report(f"{name} rep {rep}", tr_)
-                smid_report(0 if name.startswith("FULL") else 3, 128)
+                smid_report(0 if name.startswith("FULL") else 3, 128 if name.startswith("FULL") else 88, tr_)
                 if os.environ.get("PROBE_CLUSTERS"):
                     per_cluster(tr_[0] if name.startswith("FULL") else tr_[3])
             if os.environ.get("PROBE_TILES"):
