@@ -69,6 +69,8 @@ def lib():
         L.oracle_kv_bytes.restype = ctypes.c_uint64
         L.oracle_attention_recall.argtypes = [P(c_dbl), c_i64, P(c_i64), c_i64]
         L.oracle_attention_recall.restype = c_dbl
+        L.oracle_quest_reps.argtypes = [ctypes.c_void_p, c_i64, P(c_dbl)]
+        L.oracle_quest_scores.argtypes = [P(ctypes.c_float), c_i32, c_i32, c_i32, P(c_dbl), c_i64, P(c_dbl)]
         L.oracle_page_of.argtypes = [c_i64, c_i32]
         L.oracle_page_of.restype = c_i64
         L.oracle_append.argtypes = [
@@ -243,6 +245,36 @@ def attention_recall(alpha, rho) -> float:
 
 def page_of(t: int, P: int) -> int:
     return int(lib().oracle_page_of(t, P))
+
+
+def quest_reps(kv: SeqKV, s: int) -> np.ndarray:
+    """Quest page representatives [ceil(s/P)][g][2][d] (min row, max row): PAPER.md:205."""
+    out = np.empty((-(-s // kv.P), kv.g, 2, kv.d), np.float64)
+    _check(lib().oracle_quest_reps(kv.ref, s, _ptr(out, ctypes.c_double)), "quest_reps")
+    return out
+
+
+def quest_scores(q, reps) -> np.ndarray:
+    """Quest page keys (readings Q1, Q2): max_j sum_e max(q_je min_e, q_je max_e)."""
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    reps = np.ascontiguousarray(reps, dtype=np.float64)
+    m, d = q.shape
+    n_pages, g = reps.shape[0], reps.shape[1]
+    out = np.empty(n_pages, np.float64)
+    _check(lib().oracle_quest_scores(_ptr(q, ctypes.c_float), m, g, d, _ptr(reps, ctypes.c_double), n_pages,
+                                     _ptr(out, ctypes.c_double)), "quest_scores")
+    return out
+
+
+def quest_layer(cfg: "StackConfig", kv: SeqKV, q, s: int, nthreads=0):
+    """One Quest layer (reading Q3): reps -> page keys -> select (same forced set and page
+    budget as DELTA) -> attention over tokens(rho).  Returns (out, lse, keys, units, tokens)."""
+    assert cfg.select_block == cfg.page_size
+    keys = quest_scores(q, quest_reps(kv, s))
+    units = select(keys, s, cfg.select_block, cfg.n_sink, cfg.n_window, cfg.k_units)
+    tokens = units_to_tokens(units, cfg.select_block, s)
+    out, lse, _ = decode_heads(q, kv, tokens, cfg.scale, nthreads=nthreads)
+    return out, lse, keys, units, tokens
 
 
 # ---------------------------------------------------------------- the stack

@@ -264,3 +264,49 @@ double oracle_attention_recall(const double* alpha, int64_t s,
     for (int64_t t = 0; t < s; ++t) den += alpha[t];
     return num / den;
 }
+
+/* ---------------------------------------------------------------- Quest (NEXT-1) */
+
+int oracle_quest_reps(const oracle_seq_kv* kv, int64_t s, double* reps) {
+    if (!kv || s < 0) return ORACLE_ERR_USAGE;
+    const int64_t n_pages = (s + kv->P - 1) / kv->P;
+    for (int64_t u = 0; u < n_pages; ++u) {
+        for (int32_t grp = 0; grp < kv->g; ++grp) {
+            double* mn = reps + ((size_t)u * kv->g + grp) * 2 * kv->d;
+            double* mx = mn + kv->d;
+            /* element-wise extrema over the keys of page u ("element-wise min/max") */
+            for (int64_t t = u * kv->P; t < (u + 1) * kv->P && t < s; ++t) {
+                const float* k = oracle_k_row(kv, t, grp);
+                for (int32_t e = 0; e < kv->d; ++e) {
+                    if (t == u * kv->P || (double)k[e] < mn[e]) mn[e] = (double)k[e];
+                    if (t == u * kv->P || (double)k[e] > mx[e]) mx[e] = (double)k[e];
+                }
+            }
+        }
+    }
+    return ORACLE_OK;
+}
+
+int oracle_quest_scores(const float* q, int32_t m, int32_t g, int32_t d,
+                        const double* reps, int64_t n_pages, double* out) {
+    if (m < 1 || g < 1 || m % g != 0 || d < 1) return ORACLE_ERR_USAGE;
+    const int32_t gs = m / g;
+    for (int64_t u = 0; u < n_pages; ++u) {
+        double best = 0.0;
+        for (int32_t j = 0; j < m; ++j) {
+            const int32_t grp = j / gs; /* phi(j), R15 */
+            const double* mn = reps + ((size_t)u * g + grp) * 2 * d;
+            const double* mx = mn + d;
+            /* Q1: sum_e max(q_e min_e, q_e max_e) >= q . k for every key of the page */
+            double sc = 0.0;
+            for (int32_t e = 0; e < d; ++e) {
+                const double a = (double)q[(size_t)j * d + e] * mn[e];
+                const double b = (double)q[(size_t)j * d + e] * mx[e];
+                sc += a > b ? a : b;
+            }
+            if (j == 0 || sc > best) best = sc; /* Q2: max over heads */
+        }
+        out[u] = best;
+    }
+    return ORACLE_OK;
+}

@@ -130,6 +130,27 @@ uint64_t oracle_kv_bytes(uint64_t num_layers, uint64_t seq_len, uint64_t batch,
 double oracle_attention_recall(const double* alpha, int64_t s,
                                const int64_t* rho, int64_t n_rho);
 
+/* ---------------------------------------------------------------- Quest (NEXT-1)
+ * The paper's comparison policy Quest ("compresses each KV page into two
+ * representative vectors (element-wise min/max of keys), scores pages against the current
+ * query, and retrieves the top-k for attention").  Readings:
+ *   Q1 score of page u for head j = sum_e max(q_j[e] min_u[e], q_j[e] max_u[e]) with the reps
+ *      of group phi(j) (the upper bound of q . k over the page's keys; no
+ *      softmax scale — a positive factor does not change the ranking);
+ *   Q2 page key = max over the m query heads (SPEC.md:347 ledger, mirroring R7);
+ *   Q3 selection = oracle_select on the page keys (same forced sink/window pages, budget
+ *      k / P candidate pages, ties to the lowest index R9) so Quest and DELTA attend the same
+ *      number of tokens; every layer >= F selects its own pages from its own reps. */
+
+/* Page representatives: for page u < ceil(s/P) and group grp, min/max over the page's
+ * filled slots t < s of K[t][grp][e].  reps is [n_pages][g][2][d]
+ * (min row, then max row). */
+int oracle_quest_reps(const oracle_seq_kv* kv, int64_t s, double* reps);
+
+/* Page keys (Q1, Q2): out[u] = max_j sum_e max(q[j][e] min, q[j][e] max), q [m][d]. */
+int oracle_quest_scores(const float* q, int32_t m, int32_t g, int32_t d,
+                        const double* reps, int64_t n_pages, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -370,3 +370,94 @@ def test_planted_set_recovered(block, B, G):
     ranked = np.sort(keys[cand])[::-1]
     gap = (ranked[k_units - 1] - ranked[k_units]) / ranked[k_units - 1]
     assert gap > 1e-2
+
+
+# ---------------------------------------------------------------- Quest (NEXT-1)
+
+def _quest_kv(keys_sgd, P=16):
+    """A cache whose K rows are keys_sgd [s][g][d] (V = 0), identity block table."""
+    K = np.asarray(keys_sgd, np.float32)
+    return oracle.SeqKV.from_contiguous(K, np.zeros_like(K), P)
+
+
+@pytest.mark.parametrize("ex", GOLD["quest_reps"], ids=lambda e: e["cite"])
+def test_quest_reps_worked_examples(ex):
+    keys = np.asarray(ex["keys"], np.float32)[:, None, :]          # one group
+    reps = oracle.quest_reps(_quest_kv(keys, P=16), keys.shape[0])
+    assert reps.shape == (1, 1, 2, keys.shape[2])
+    assert np.array_equal(reps[0, 0, 0], ex["min"]) and np.array_equal(reps[0, 0, 1], ex["max"])
+
+
+@pytest.mark.parametrize("ex", GOLD["quest_score"], ids=lambda e: e["cite"])
+def test_quest_score_worked_examples(ex):
+    reps = np.asarray([[[ex["min"], ex["max"]]]], np.float64)       # [1 page][1 group][2][d]
+    got = oracle.quest_scores(np.asarray([ex["q"]], np.float32), reps)
+    assert got[0] == ex["score"]
+
+
+def test_quest_reps_pages_and_partial_last_page():
+    """Per-page extrema over exactly the page's filled slots: a 37-token cache has pages of
+    16, 16 and 5 tokens; a value planted in slot 5 of the last page (t = 37, not yet written)
+    must not count."""
+    rng = np.random.default_rng(5)
+    s, g, d, P = 37, 2, 8, 16
+    K = rng.integers(-50, 50, size=(48, g, d)).astype(np.float32)
+    K[37, :, :] = 1000.0                                             # beyond s
+    reps = oracle.quest_reps(_quest_kv(K, P), s)
+    assert reps.shape == (3, g, 2, d)
+    for u, (lo, hi) in enumerate([(0, 16), (16, 32), (32, 37)]):
+        for grp in range(g):
+            for e in range(d):
+                col = [float(K[t, grp, e]) for t in range(lo, hi)]
+                assert reps[u, grp, 0, e] == min(col) and reps[u, grp, 1, e] == max(col)
+
+
+def test_quest_upper_bound_property():
+    """quest_score(q, reps(page)) >= max over the page's keys of q . k, for every
+    head (m = 1 so the page key is that head's bound), over 2000 random (q, page) draws; and the
+    bound is attained when the page holds a single distinct key."""
+    rng = np.random.default_rng(6)
+    P, d = 16, 16
+    for _ in range(2000):
+        n = int(rng.integers(1, P + 1))
+        K = rng.standard_normal((P, 1, d)).astype(np.float32)
+        q = rng.standard_normal((1, d)).astype(np.float32)
+        bound = oracle.quest_scores(q, oracle.quest_reps(_quest_kv(K, P), n))[0]
+        best = max(float(np.dot(q[0].astype(np.float64), K[t, 0].astype(np.float64))) for t in range(n))
+        assert bound >= best - 1e-12
+    K = np.repeat(rng.standard_normal((1, 1, d)).astype(np.float32), P, axis=0)
+    q = rng.standard_normal((1, d)).astype(np.float32)
+    bound = oracle.quest_scores(q, oracle.quest_reps(_quest_kv(K, P), P))[0]
+    assert abs(bound - float(np.dot(q[0].astype(np.float64), K[0, 0].astype(np.float64)))) < 1e-12
+
+
+def test_quest_max_over_heads_and_group_map():
+    """Q2 + R15: m = 4 heads over g = 2 groups (heads 0,1 -> group 0; 2,3 -> group 1).  Page 0's
+    group-1 keys align with head 3's query, page 1's group-0 keys with head 0's: each page's key
+    is the best head's bound, and permuting heads within a group leaves the keys unchanged."""
+    d, P = 4, 16
+    K = np.zeros((2 * P, 2, d), np.float32)
+    K[:P, 1, :] = [0, 0, 5, 0]           # page 0, group 1
+    K[P:, 0, :] = [2, 0, 0, 0]           # page 1, group 0
+    q = np.zeros((4, d), np.float32)
+    q[3] = [0, 0, 1, 0]
+    q[0] = [1, 0, 0, 0]
+    keys = oracle.quest_scores(q, oracle.quest_reps(_quest_kv(K, P), 2 * P))
+    assert keys.tolist() == [5.0, 2.0]
+    keys2 = oracle.quest_scores(q[[1, 0, 3, 2]], oracle.quest_reps(_quest_kv(K, P), 2 * P))
+    assert keys2.tolist() == keys.tolist()
+
+
+def test_quest_dominant_page_selected_and_budget_all():
+    """SPEC.md:327-329: a page whose keys all equal q is picked first among the older pages;
+    a page budget covering every candidate selects every page (R12)."""
+    rng = np.random.default_rng(7)
+    P, d, s = 16, 8, 16 * 12
+    K = (0.1 * rng.standard_normal((s, 1, d))).astype(np.float32)
+    q = rng.standard_normal((1, d)).astype(np.float32)
+    K[5 * P:6 * P, 0, :] = q[0]
+    kv = _quest_kv(K, P)
+    keys = oracle.quest_scores(q, oracle.quest_reps(kv, s))
+    units = oracle.select(keys, s, P, 4, 32, 1)                      # sink page 0 + 2 window pages + 1
+    assert units.tolist() == [0, 5, 10, 11]
+    assert oracle.select(keys, s, P, 4, 32, 9).tolist() == list(range(12))
