@@ -49,7 +49,17 @@ typedef enum {
 
 typedef enum { DELTA_BF16 = 0, DELTA_FP32 = 1 } delta_dtype;
 
-typedef enum { DELTA_ROLE_FULL = 0, DELTA_ROLE_SELECT = 1, DELTA_ROLE_SPARSE = 2 } delta_role;
+typedef enum { DELTA_ROLE_FULL = 0, DELTA_ROLE_SELECT = 1, DELTA_ROLE_SPARSE = 2, DELTA_ROLE_QUEST = 3 } delta_role;
+
+/* Selection policy of the layers >= F.
+ *  DELTA: the paper's three-tier schedule (Delta layers select, sparse layers reuse).
+ *  QUEST: the paper's comparison system Quest: every layer >= F
+ *         (role QUEST) keeps the element-wise min/max of the keys of each (page, kv head) and, at
+ *         every decode, scores each page by max_j sum_e max(q_j[e] min[e], q_j[e] max[e]) (Q1, Q2:
+ *         an upper bound of q_j . k over the page), selects the forced sink/window pages plus the
+ *         top budget_k/P candidate pages with the same rule as DELTA (Q3) and attends to them.
+ *         Needs num_select_layers == 0, select_block == page_size, kv_dtype BF16, shard_world 1. */
+typedef enum { DELTA_POLICY_DELTA = 0, DELTA_POLICY_QUEST = 1 } delta_policy;
 
 /* Problem statement of the method (PAPER.md:157-158 schedule, 168-171/185 budget and
  * window, 180-181/196 paged layout). */
@@ -87,6 +97,7 @@ typedef struct {
                                   after the local pass and the caller moves the bytes itself
                                   (delta_shard_exchange_buffers) and calls delta_shard_merge /
                                   delta_shard_select_merge (used for single-GPU simulation). */
+    int32_t policy;            /* delta_policy (0 = DELTA) */
 } delta_config;
 
 /* Caller-owned device buffers.  Sizes from delta_query_sizes. */
@@ -178,6 +189,27 @@ delta_status delta_decode_step(delta_t h, int32_t batch, const void* q_all, cons
 delta_status delta_decode_step_host(delta_t h, int32_t batch, const void* q_all_host,
                                     const void* k_all_host, const void* v_all_host,
                                     float* out_all_host, cudaStream_t stream);
+
+/* ---- Quest policy (policy == DELTA_POLICY_QUEST) ------------------------------------
+ * Page representatives are kept in the workspace, [L][num_phys_pages][g][2][d] bf16 (min row,
+ * then max row, of the keys of each (physical page, kv head)), updated by every append
+ * (delta_append_kv / the append inside delta_append_decode_layer / delta_decode_step).  After
+ * filling the pool some other way (external prefill), rebuild them for pages < ceil(n_b/P) of
+ * sequences [0, batch) of one layer (layer >= 0) or of every QUEST layer (layer == -1).
+ * A QUEST layer's delta_decode_layer / delta_append_decode_layer runs: [append + reps update],
+ * page keys, top-k (select.cu), sparse attention over the plan — four launches. */
+delta_status delta_quest_build_reps(delta_t h, int32_t layer, int32_t batch, cudaStream_t stream);
+
+/* Test hook: device copy of the plan that `layer` attends (a Delta layer's plan, the plan of
+ * the governing Delta layer of a SPARSE layer, or a QUEST layer's own plan from its latest
+ * decode): idx_out [batch][plan_capacity] (entries past count unspecified), count_out [batch]. */
+delta_status delta_copy_plan(delta_t h, int32_t layer, int32_t batch, int32_t* idx_out, int32_t* count_out,
+                             cudaStream_t stream);
+
+/* Test hook: device pointers into the workspace.  which = 0: unit keys of the latest selection
+ * [max_batch][ceil(max_seq_len/select_block)] fp32; which = 1: Quest page representatives
+ * (layout above).  *bytes = size of the region. */
+delta_status delta_workspace_region(delta_t h, int32_t which, void** ptr, size_t* bytes);
 
 /* Synchronises `stream`, reads and clears the sticky device error flag.
  * *sticky = DELTA_OK or the first device-side error recorded. The only syncing call. */

@@ -18,7 +18,8 @@ LIB_PATH = os.environ.get("DELTA_LIB_PATH") or os.path.join(_HERE, "libdelta.so"
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "delta.h")
 
 DELTA_BF16, DELTA_FP32 = 0, 1
-ROLE_FULL, ROLE_SELECT, ROLE_SPARSE = 0, 1, 2
+ROLE_FULL, ROLE_SELECT, ROLE_SPARSE, ROLE_QUEST = 0, 1, 2, 3
+POLICY_DELTA, POLICY_QUEST = 0, 1
 STATUS = {0: "OK", 1: "CONFIG", 2: "USAGE", 3: "NUMERIC", 4: "CAPACITY", 5: "CUDA", 6: "NCCL"}
 
 
@@ -37,6 +38,7 @@ class _Config(ctypes.Structure):
         ("budget_k", ctypes.c_int32), ("n_sink", ctypes.c_int32), ("n_window", ctypes.c_int32),
         ("select_block", ctypes.c_int32), ("kv_dtype", ctypes.c_int), ("softmax_scale", ctypes.c_float),
         ("shard_world", ctypes.c_int32), ("shard_rank", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
+        ("policy", ctypes.c_int32),
     ]
 
 
@@ -104,6 +106,12 @@ def load_library() -> ctypes.CDLL:
     L.delta_shard_merge.restype = st
     L.delta_shard_select_merge.argtypes = [vp, i32, i32, vp, vp, vp]
     L.delta_shard_select_merge.restype = st
+    L.delta_quest_build_reps.argtypes = [vp, i32, i32, vp]
+    L.delta_quest_build_reps.restype = st
+    L.delta_copy_plan.argtypes = [vp, i32, i32, vp, vp, vp]
+    L.delta_copy_plan.restype = st
+    L.delta_workspace_region.argtypes = [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)]
+    L.delta_workspace_region.restype = st
     _lib = L
     return L
 
@@ -137,6 +145,7 @@ class DeltaConfig:
     shard_world: int = 1
     shard_rank: int = 0
     nccl_id: bytes | None = None   # 128 bytes from nccl_unique_id() (rank 0), or None
+    policy: int = POLICY_DELTA
 
     def to_c(self):
         arr = (ctypes.c_int32 * max(1, len(self.select_layers)))(*self.select_layers)
@@ -145,7 +154,7 @@ class DeltaConfig:
                     self.max_seq_len, self.page_size, self.num_phys_pages, self.num_full_prefix,
                     len(self.select_layers), arr, self.budget_k, self.n_sink, self.n_window, self.select_block,
                     self.kv_dtype, self.softmax_scale, self.shard_world, self.shard_rank,
-                    ctypes.cast(nid, ctypes.c_void_p) if nid is not None else None)
+                    ctypes.cast(nid, ctypes.c_void_p) if nid is not None else None, self.policy)
         return c, (arr, nid)  # keep alive
 
     @property
@@ -266,6 +275,19 @@ class DeltaStack:
     def select(self, layer: int, batch: int, keys_override=None, idx_out=None, count_out=None, stream=None):
         _check(self.lib.delta_select(self.h, layer, batch, _ptr(keys_override), _ptr(idx_out), _ptr(count_out),
                                      _stream(stream)), self.h)
+
+    def quest_build_reps(self, layer: int = -1, batch: int | None = None, stream=None):
+        _check(self.lib.delta_quest_build_reps(self.h, layer, batch or self.cfg.max_batch, _stream(stream)), self.h)
+
+    def copy_plan(self, layer: int, batch: int, idx_out, count_out, stream=None):
+        _check(self.lib.delta_copy_plan(self.h, layer, batch, _ptr(idx_out), _ptr(count_out), _stream(stream)),
+               self.h)
+
+    def workspace_region(self, which: int):
+        """(device pointer, bytes) of a workspace region (0 unit keys, 1 Quest reps)."""
+        ptr, n = ctypes.c_void_p(), ctypes.c_size_t()
+        _check(self.lib.delta_workspace_region(self.h, which, ctypes.byref(ptr), ctypes.byref(n)), self.h)
+        return ptr.value, n.value
 
     def decode_step(self, q_all, k_all, v_all, out_all, lse_all=None, stream=None):
         _check(self.lib.delta_decode_step(self.h, q_all.shape[1], q_all.data_ptr(), k_all.data_ptr(),

@@ -36,6 +36,35 @@ __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
         *reinterpret_cast<uint4*>(pool + dst_off + (size_t)kPage * row_bytes) =
             *reinterpret_cast<const uint4*>(vs + src_off);
     }
+    // Quest page representatives (quest.cu): thread owns (head, bf16 pair) and folds the
+    // appended tokens in order; a token in slot 0 starts its page's min/max.
+    if (p.reps) {
+        const int pairs = p.d / 2;
+        const __nv_bfloat162* kn = reinterpret_cast<const __nv_bfloat162*>(ks);
+        for (int i = threadIdx.x; i < p.g * pairs; i += blockDim.x) {
+            const int hh = i / pairs, e2 = i - hh * pairs;
+            int cur = -1;
+            __nv_bfloat162 mn, mx;
+            __nv_bfloat162* rep = nullptr;
+            for (int tok = 0; tok < p.ntok; ++tok) {
+                const int t = n + tok, u = t / kPage;
+                if (u < p.page_lo || u >= p.page_hi) continue;
+                const __nv_bfloat162 k = kn[((size_t)tok * p.g + hh) * pairs + e2];
+                if (u != cur) {
+                    if (rep) { rep[e2] = mn; rep[pairs + e2] = mx; }
+                    rep = reinterpret_cast<__nv_bfloat162*>(p.reps) +
+                          (((size_t)p.layer * p.num_phys + bt[u]) * p.g + hh) * p.d;
+                    cur = u;
+                    if (t % kPage == 0) { mn = k; mx = k; }
+                    else { mn = __hmin2(rep[e2], k); mx = __hmax2(rep[pairs + e2], k); }
+                } else {
+                    mn = __hmin2(mn, k);
+                    mx = __hmax2(mx, k);
+                }
+            }
+            if (rep) { rep[e2] = mn; rep[pairs + e2] = mx; }
+        }
+    }
     __syncthreads();
     if (threadIdx.x == 0) p.seq_len[p.layer * p.max_batch + b] = (n + p.ntok) * p.g;
 }

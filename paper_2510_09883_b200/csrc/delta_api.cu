@@ -29,7 +29,8 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
     size_t seq_len, err, cnt_sel, logits, lse_buf, keys, plan_idx, plan_phys, plan_count, plan_stamp, plan_lo, plan_hi,
-        shard_send, shard_recv, cand_send, cand_recv, stage_q, stage_k, stage_v, stage_out, gpart, gcnt, total;
+        shard_send, shard_recv, cand_send, cand_recv, stage_q, stage_k, stage_v, stage_out, gpart, gcnt, reps,
+        reps_bytes, total;
     int gslots;  // split partial slots of the global-merge kernels
     size_t shard_block, cand_block;  // bytes of one rank's attention partial / candidate block
     int max_units, plan_cap, n_delta, max_pages;
@@ -106,6 +107,21 @@ std::string validate(const delta_config& c, std::vector<int>& role, std::vector<
     if (c.shard_world < 1 || c.shard_world > 64 || c.shard_rank < 0 || c.shard_rank >= c.shard_world)
         return "shard_world must be in [1, 64] and 0 <= shard_rank < shard_world";
     if (c.softmax_scale < 0.f || !std::isfinite(c.softmax_scale)) return "softmax_scale must be finite and >= 0";
+    if (c.policy != DELTA_POLICY_DELTA && c.policy != DELTA_POLICY_QUEST) return "policy must be DELTA or QUEST";
+    if (c.policy == DELTA_POLICY_QUEST) {
+        // Quest: every layer >= F selects its own pages (readings Q1-Q3)
+        if (c.num_select_layers != 0) return "QUEST policy takes no Delta layers";
+        if (c.select_block != c.page_size) return "QUEST selects pages: select_block must be page_size";
+        if (c.kv_dtype != DELTA_BF16) return "QUEST needs bf16 KV";
+        if (c.shard_world != 1) return "QUEST is not sequence-sharded";
+        role.assign(c.num_layers, kRoleQuest);
+        gov.assign(c.num_layers, 0);
+        for (int l = 0; l < c.num_layers; ++l) {
+            if (l < c.num_full_prefix) role[l] = kRoleFull;
+            gov[l] = l;
+        }
+        return "";
+    }
     role.assign(c.num_layers, kRoleSparse);
     gov.assign(c.num_layers, -1);
     for (int i = 0; i < c.num_select_layers; ++i) {
@@ -147,7 +163,7 @@ Layout layout(const delta_config& c, int sms) {
         const int win_units = c.n_window > 0 ? (blk == 1 ? c.n_window : (c.n_window - 1) / blk + 2) : 0;
         L.plan_cap = std::max(1, std::min(L.max_units, k_units + sink_units + win_units));
     }
-    const bool has_sel = c.num_select_layers > 0;
+    const bool has_sel = c.num_select_layers > 0 || c.policy == DELTA_POLICY_QUEST;  // keys + plan
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + std::max<size_t>(bytes, 1)); return o; };
     L.seq_len = take((size_t)c.num_layers * c.max_batch * 4);
@@ -156,7 +172,7 @@ Layout layout(const delta_config& c, int sms) {
     L.logits = take(has_sel ? (size_t)c.max_batch * c.max_seq_len * m * 4 : 0);
     L.lse_buf = take((size_t)c.max_batch * m * 4);
     L.keys = take(has_sel ? (size_t)c.max_batch * L.max_units * 4 : 0);
-    const int nd = std::max(1, L.n_delta);
+    const int nd = std::max(1, L.n_delta);  // (QUEST: n_delta = 0, slot 0 = the current layer's plan)
     L.plan_idx = take((size_t)nd * c.max_batch * L.plan_cap * 4);
     L.plan_phys = take((size_t)nd * c.max_batch * L.plan_cap * 4);
     L.plan_count = take((size_t)nd * c.max_batch * 4);
@@ -179,6 +195,11 @@ Layout layout(const delta_config& c, int sms) {
     L.gslots = std::max(sms, 1) * 2;  // batch * g * nsplit <= sms for every gmerge launch
     L.gpart = take((size_t)L.gslots * gpart_floats(D) * 4);
     L.gcnt = take((size_t)c.max_batch * g * kMaxSplitG * 8);  // ticket counter per (b, h, split count)
+    {   // Quest page representatives [L][num_phys][g][2][d] bf16
+        const long long phys = c.num_phys_pages > 0 ? c.num_phys_pages : (long long)c.max_batch * L.max_pages;
+        L.reps_bytes = c.policy == DELTA_POLICY_QUEST ? (size_t)c.num_layers * phys * g * 2 * D * 2 : 0;
+        L.reps = take(L.reps_bytes);
+    }
     L.total = off;
     return L;
 }
@@ -312,7 +333,8 @@ AttnParams attn_params(delta_ctx* h, int layer, int batch) {
     const delta_config& c = h->cfg;
     AttnParams p = {};
     p.m = c.num_q_heads; p.g = c.num_kv_heads; p.gs = h->gs; p.d = c.head_dim;
-    p.layer = layer; p.batch = batch; p.role = h->role[layer];
+    p.layer = layer; p.batch = batch;
+    p.role = h->role[layer] == kRoleQuest ? kRoleSparse : h->role[layer];  // a Quest layer attends its plan
     p.num_phys = c.num_phys_pages; p.bt_stride = h->L.max_pages;
     p.max_batch = c.max_batch; p.max_seq = c.max_seq_len;
     p.sel_block = c.select_block; p.plan_cap = h->L.plan_cap;
@@ -406,8 +428,58 @@ delta_status launch_merge(delta_ctx* h, int layer, int batch, float* out, float*
     return DELTA_OK;
 }
 
+QuestParams quest_params(delta_ctx* h, int layer, int batch, const void* q) {
+    const delta_config& c = h->cfg;
+    QuestParams p = {};
+    p.m = c.num_q_heads; p.g = c.num_kv_heads; p.d = c.head_dim; p.layer = layer; p.batch = batch;
+    p.num_phys = c.num_phys_pages; p.bt_stride = h->L.max_pages; p.max_batch = c.max_batch;
+    p.max_units = h->L.max_units;
+    p.kv_pool = h->kv_pool; p.reps = h->ws + h->L.reps; p.block_table = h->block_table;
+    p.seq_len = h->at<int32_t>(h->L.seq_len); p.q = q; p.keys = h->at<float>(h->L.keys);
+    return p;
+}
+
+delta_status launch_append_impl(delta_ctx* h, int layer, int batch, int ntok, const void* k_new, const void* v_new,
+                                cudaStream_t st) {
+    AppendParams p = {};
+    p.g = h->cfg.num_kv_heads; p.d = h->cfg.head_dim; p.layer = layer; p.batch = batch; p.ntok = ntok;
+    p.num_phys = h->cfg.num_phys_pages; p.bt_stride = h->L.max_pages; p.max_batch = h->cfg.max_batch;
+    p.max_seq = h->cfg.max_seq_len; p.elem_bytes = elem_bytes(h->cfg);
+    p.k_new = k_new; p.v_new = v_new; p.kv_pool = h->kv_pool;
+    p.reps = h->role[layer] == kRoleQuest ? h->ws + h->L.reps : nullptr;
+    p.block_table = h->block_table; p.seq_len = h->at<int32_t>(h->L.seq_len); p.err = h->at<int32_t>(h->L.err);
+    p.page_lo = h->page_lo; p.page_hi = h->page_hi;
+    cudaError_t e = launch_append(p, st, h->pdl);
+    if (e != cudaSuccess) return cuda_fail(h, e, "append launch");
+    ++h->launches;
+    h->last_kind = delta_ctx::kLastAppend;
+    h->last_layer = layer;
+    return DELTA_OK;
+}
+
+delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_override, int32_t* idx_out,
+                        int32_t* count_out, cudaStream_t st, int shard_mode);
+
+// A Quest layer before its attention: [append + reps update], page keys, top-k -> plan slot 0.
+delta_status launch_quest_select(delta_ctx* h, int layer, int batch, const void* k_new, const void* v_new,
+                                 const void* q, cudaStream_t st) {
+    if (k_new) {
+        delta_status s = launch_append_impl(h, layer, batch, 1, k_new, v_new, st);
+        if (s != DELTA_OK) return s;
+    }
+    cudaError_t e = launch_quest_score(quest_params(h, layer, batch, q), h->L.max_pages, h->sms, st, h->pdl);
+    if (e != cudaSuccess) return cuda_fail(h, e, "quest score launch");
+    ++h->launches;
+    return launch_sel(h, layer, batch, h->at<float>(h->L.keys), nullptr, nullptr, st, 0);
+}
+
 delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new, const void* v_new,
                            const void* q, float* out, float* lse_out, cudaStream_t st, bool in_step = false) {
+    if (h->role[layer] == kRoleQuest) {
+        delta_status s = launch_quest_select(h, layer, batch, k_new, v_new, q, st);
+        if (s != DELTA_OK) return s;
+        k_new = v_new = nullptr;  // appended above
+    }
     AttnParams p = attn_params(h, layer, batch);
     p.q = q; p.out = out; p.lse_out = lse_out;
     p.fuse_append = (k_new != nullptr);
@@ -443,7 +515,7 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
 }
 
 delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_override, int32_t* idx_out,
-                        int32_t* count_out, cudaStream_t st, int shard_mode = 0) {
+                        int32_t* count_out, cudaStream_t st, int shard_mode) {
     const delta_config& c = h->cfg;
     SelectParams p = {};
     const int sl = h->slot[layer];
@@ -520,7 +592,7 @@ delta_status enqueue_step(delta_ctx* h, int batch, const void* q_all, const void
         if (s != DELTA_OK) return s;
         if (h->role[l] == kRoleSelect) {
             s = h->world > 1 ? launch_sel_sharded(h, l, batch, nullptr, nullptr, st)
-                             : launch_sel(h, l, batch, nullptr, nullptr, nullptr, st);
+                             : launch_sel(h, l, batch, nullptr, nullptr, nullptr, st, 0);
             if (s != DELTA_OK) return s;
         }
     }
@@ -570,6 +642,8 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
     h->role = role; h->gov = gov;
     h->slot.assign(cfg->num_layers, -1);
     for (int i = 0; i < cfg->num_select_layers; ++i) h->slot[cfg->select_layers[i]] = i;
+    for (int l = 0; l < cfg->num_layers; ++l)
+        if (h->role[l] == kRoleQuest) h->slot[l] = 0;  // each Quest layer's own plan, consumed at once
     h->sms = num_sms_current();
     h->gs = cfg->num_q_heads / cfg->num_kv_heads;
     h->L = layout(h->cfg, h->sms);
@@ -710,20 +784,9 @@ delta_status delta_append_kv(delta_t h, int32_t layer, int32_t batch, int32_t nt
     delta_status s = check_layer_batch(h, layer, batch);
     if (s != DELTA_OK) return s;
     if (ntok < 1 || !k_new || !v_new) return fail(h, DELTA_ERR_USAGE, "bad ntok or null k_new/v_new");
-    AppendParams p = {};
-    p.g = h->cfg.num_kv_heads; p.d = h->cfg.head_dim; p.layer = layer; p.batch = batch; p.ntok = ntok;
-    p.num_phys = h->cfg.num_phys_pages; p.bt_stride = h->L.max_pages; p.max_batch = h->cfg.max_batch;
-    p.max_seq = h->cfg.max_seq_len; p.elem_bytes = elem_bytes(h->cfg);
-    p.k_new = k_new; p.v_new = v_new; p.kv_pool = h->kv_pool;
-    p.block_table = h->block_table; p.seq_len = h->at<int32_t>(h->L.seq_len); p.err = h->at<int32_t>(h->L.err);
-    p.page_lo = h->page_lo; p.page_hi = h->page_hi;
-    cudaError_t e = launch_append(p, stream, h->pdl);
-    if (e != cudaSuccess) return cuda_fail(h, e, "append launch");
-    ++h->launches;
-    h->last_kind = delta_ctx::kLastAppend;
-    h->last_layer = layer;
-    h->step[layer] += 1;
-    return DELTA_OK;
+    s = launch_append_impl(h, layer, batch, ntok, k_new, v_new, stream);
+    if (s == DELTA_OK) h->step[layer] += 1;
+    return s;
 }
 
 delta_status delta_decode_layer(delta_t h, int32_t layer, int32_t batch, const void* q, float* out,
@@ -765,7 +828,7 @@ delta_status delta_select(delta_t h, int32_t layer, int32_t batch, const float* 
         s = keys_override ? launch_sel(h, layer, batch, keys_override, idx_out, count_out, stream, 2)
                           : launch_sel_sharded(h, layer, batch, idx_out, count_out, stream);
     else
-        s = launch_sel(h, layer, batch, keys_override, idx_out, count_out, stream);
+        s = launch_sel(h, layer, batch, keys_override, idx_out, count_out, stream, 0);
     if (s == DELTA_OK) h->sel_step[h->slot[layer]] = h->step[layer];
     return s;
 }
@@ -838,6 +901,56 @@ delta_status delta_decode_step_host(delta_t h, int32_t batch, const void* q_all_
     if (s != DELTA_OK) return s;
     err = cudaMemcpyAsync(out_all_host, dout, ob, cudaMemcpyDeviceToHost, stream);
     if (err != cudaSuccess) return cuda_fail(h, err, "step_host D2H");
+    return DELTA_OK;
+}
+
+delta_status delta_quest_build_reps(delta_t h, int32_t layer, int32_t batch, cudaStream_t stream) {
+    if (!h) return fail(nullptr, DELTA_ERR_USAGE, "null handle");
+    if (h->cfg.policy != DELTA_POLICY_QUEST) return fail(h, DELTA_ERR_USAGE, "not a QUEST handle");
+    if (batch < 1 || batch > h->cfg.max_batch) return fail(h, DELTA_ERR_USAGE, "batch out of range");
+    if (layer < -1 || layer >= h->cfg.num_layers) return fail(h, DELTA_ERR_USAGE, "layer out of range");
+    const int l0 = layer < 0 ? 0 : layer, l1 = layer < 0 ? h->cfg.num_layers : layer + 1;
+    for (int l = l0; l < l1; ++l) {
+        if (h->role[l] != kRoleQuest) continue;
+        cudaError_t e = launch_quest_reps(quest_params(h, l, batch, nullptr), h->L.max_pages, stream, h->pdl);
+        if (e != cudaSuccess) return cuda_fail(h, e, "quest reps launch");
+        ++h->launches;
+        h->last_kind = delta_ctx::kLastAppend;
+        h->last_layer = l;
+    }
+    return DELTA_OK;
+}
+
+delta_status delta_copy_plan(delta_t h, int32_t layer, int32_t batch, int32_t* idx_out, int32_t* count_out,
+                             cudaStream_t stream) {
+    delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    if (h->role[layer] == kRoleFull) return fail(h, DELTA_ERR_USAGE, "a FULL layer has no plan");
+    const int sl = h->slot[h->gov[layer]];
+    const size_t cap = h->L.plan_cap, mb = h->cfg.max_batch;
+    cudaError_t e = cudaSuccess;
+    if (idx_out)
+        e = cudaMemcpyAsync(idx_out, h->at<int32_t>(h->L.plan_idx) + sl * mb * cap, batch * cap * 4,
+                            cudaMemcpyDeviceToDevice, stream);
+    if (e == cudaSuccess && count_out)
+        e = cudaMemcpyAsync(count_out, h->at<int32_t>(h->L.plan_count) + sl * mb, batch * 4, cudaMemcpyDeviceToDevice,
+                            stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "copy_plan");
+    h->last_kind = delta_ctx::kLastNone;  // a copy node sits between kernels
+    return DELTA_OK;
+}
+
+delta_status delta_workspace_region(delta_t h, int32_t which, void** ptr, size_t* bytes) {
+    if (!h || !ptr || !bytes) return fail(h, DELTA_ERR_USAGE, "null argument");
+    if (which == 0) {
+        *ptr = h->ws + h->L.keys;
+        *bytes = (size_t)h->cfg.max_batch * h->L.max_units * 4;
+    } else if (which == 1) {
+        *ptr = h->ws + h->L.reps;
+        *bytes = h->L.reps_bytes;
+    } else {
+        return fail(h, DELTA_ERR_USAGE, "unknown workspace region");
+    }
     return DELTA_OK;
 }
 

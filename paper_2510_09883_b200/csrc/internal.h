@@ -7,7 +7,7 @@
 
 namespace delta {
 
-enum Role : int { kRoleFull = 0, kRoleSelect = 1, kRoleSparse = 2 };
+enum Role : int { kRoleFull = 0, kRoleSelect = 1, kRoleSparse = 2, kRoleQuest = 3 };  // Quest: host role only
 enum DevErr : int { kDevOk = 0, kDevUsage = 2, kDevNumeric = 3, kDevCapacity = 4 };
 
 constexpr int kPage = 16;        // P
@@ -116,6 +116,7 @@ struct ShardMergeParams {
 
 struct AppendParams {
     int g, d, layer, batch, ntok, num_phys, bt_stride, max_batch, max_seq, elem_bytes;
+    void* reps;         // Quest layers: [L][num_phys][g][2][d] bf16 page min/max, updated per token
     int page_lo, page_hi;  // sequence sharding: this rank writes rows on its pages only
     const void* k_new;  // [batch][ntok][g][d]
     const void* v_new;
@@ -124,6 +125,19 @@ struct AppendParams {
     int32_t* seq_len;
     int32_t* err;
 };
+
+// Quest policy (quest.cu): page representatives and page keys of one layer.
+struct QuestParams {
+    int m, g, d, layer, batch, num_phys, bt_stride, max_batch, max_units;
+    const void* kv_pool;        // [L][num_phys][g][2][P][d] bf16
+    void* reps;                 // [L][num_phys][g][2][d] bf16 (min row, max row)
+    const int32_t* block_table;
+    const int32_t* seq_len;     // raw counters n * g
+    const void* q;              // [batch][m][d] bf16
+    float* keys;                // [max_batch][max_units] page keys
+};
+cudaError_t launch_quest_reps(const QuestParams& p, int max_pages, cudaStream_t st, bool pdl);
+cudaError_t launch_quest_score(const QuestParams& p, int max_pages, int sms, cudaStream_t st, bool pdl);
 
 // Launchers (attn_tc.cu / attn_simt.cu / select.cu / append.cu).  Each returns the
 // cudaError_t of the launch.  `pdl` enables programmatic dependent launch.
