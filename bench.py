@@ -252,13 +252,15 @@ def run_ours(args, c):
     max_seq = s_first + K + PAGE
     seed = 2511 if seq_shard else 2511 + 1000 * rank  # batch sharding: every rank its own sequences
 
-    def make_cfg(full: bool):
+    def make_cfg(full: bool, quest: bool = False):
         return d200.DeltaConfig(num_layers=c["L"], num_q_heads=c["m"], num_kv_heads=c["g"], head_dim=c["d"],
                                 max_batch=batch, max_seq_len=max_seq,
-                                num_full_prefix=c["L"] if full else c["F"], select_layers=[] if full else c["delta"],
+                                num_full_prefix=c["L"] if full else c["F"],
+                                select_layers=[] if (full or quest) else c["delta"],
                                 budget_k=c["k"], n_sink=S_SINK, n_window=L_WIN, select_block=PAGE,
                                 shard_world=world if seq_shard else 1, shard_rank=rank if seq_shard else 0,
-                                nccl_id=nccl_ids[1 if full else 0])
+                                nccl_id=nccl_ids[1 if full else 0],
+                                policy=d200.POLICY_QUEST if quest else d200.POLICY_DELTA)
 
     cfg = make_cfg(False)
     bt = torch.from_numpy(synth.block_table(seed, batch, cfg.max_pages))
@@ -268,8 +270,19 @@ def run_ours(args, c):
     _, fws = d200.query_sizes(fcfg)
     full = d200.DeltaStack(fcfg, delta.kv_pool, delta.block_table,
                            torch.zeros(fws, dtype=torch.uint8, device=dev))
+    # the paper's comparison policy Quest (NEXT-1) on the same pools: every layer >= F selects
+    # its own pages from min/max key representatives (its own workspace)
+    quest = None
+    if not seq_shard:
+        qcfg = make_cfg(False, quest=True)
+        _, qws = d200.query_sizes(qcfg)
+        quest = d200.DeltaStack(qcfg, delta.kv_pool, delta.block_table,
+                                torch.zeros(qws, dtype=torch.uint8, device=dev))
     t0 = time.time()
     sd.fill_pools(delta.kv_pool, delta.block_table, seed, s_pre, batch, range(c["L"]))
+    if quest is not None:
+        quest.set_seq_lens([s_pre] * batch)
+        quest.quest_build_reps(-1, batch)
     torch.cuda.synchronize()
     log(f"[rank {rank}] filled {delta.kv_pool.numel() * 2 / 2**30:.1f} GiB KV in {time.time() - t0:.1f}s "
         f"(batch {batch}, s_pre {s_pre})")
@@ -317,6 +330,7 @@ def run_ours(args, c):
     clocks = ClockSampler(local)
     ms_delta, launches, clk = time_stack(delta, clocks)
     ms_full, _, _ = time_stack(full)
+    ms_quest = time_stack(quest)[0] if quest is not None else None
     err = delta.get_error()
     assert err == 0, f"device error flag {err}"
 
@@ -330,6 +344,8 @@ def run_ours(args, c):
 
     ms_delta = max_over_ranks(ms_delta)
     ms_full = max_over_ranks(ms_full)
+    if ms_quest is not None:
+        ms_quest = max_over_ranks(ms_quest)
 
     # algorithmic bytes over the timed steps (s grows by one per step)
     byts_delta = byts_full = 0
@@ -415,7 +431,8 @@ def run_ours(args, c):
     }
     if rank == 0:
         log(f"DELTA {1e3 * ms_delta / K:.1f} us/step, Full {1e3 * ms_full / K:.1f} us/step, "
-            f"speedup {ms_full / ms_delta:.3f}x; kernels {kernels}")
+            f"speedup {ms_full / ms_delta:.3f}x; Quest {1e3 * ms_quest / K if ms_quest else 0:.1f} us/step; "
+            f"kernels {kernels}")
 
     if rank != 0:
         if world > 1:
@@ -443,6 +460,8 @@ def run_ours(args, c):
         "decode_step_us": round(1e3 * ms_delta / K, 2),
         "full_stack_us": round(1e3 * ms_full / K, 2),
         "speedup_vs_full": round(ms_full / ms_delta, 3),
+        "quest_stack_us": round(1e3 * ms_quest / K, 2) if ms_quest else None,
+        "quest_speedup_vs_full": round(ms_full / ms_quest, 3) if ms_quest else None,
         "byte_ratio": round(byte_ratio, 3),
         "speedup_target": round(0.8 * byte_ratio, 3),
         "full_stack_gbs": round(byts_full * (1 if seq_shard else world) / (ms_full * 1e-3) / 1e9, 2),

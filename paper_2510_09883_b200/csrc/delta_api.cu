@@ -458,19 +458,18 @@ delta_status launch_append_impl(delta_ctx* h, int layer, int batch, int ntok, co
 }
 
 delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_override, int32_t* idx_out,
-                        int32_t* count_out, cudaStream_t st, int shard_mode);
+                        int32_t* count_out, cudaStream_t st, int shard_mode, const void* k_new = nullptr,
+                        const void* v_new = nullptr);
 
-// A Quest layer before its attention: [append + reps update], page keys, top-k -> plan slot 0.
+// A Quest layer before its attention: page keys over the pages before this step's token (its
+// page is a forced window page), then one launch that appends the token (pool rows, reps,
+// length) and ranks the pages -> plan slot 0.
 delta_status launch_quest_select(delta_ctx* h, int layer, int batch, const void* k_new, const void* v_new,
                                  const void* q, cudaStream_t st) {
-    if (k_new) {
-        delta_status s = launch_append_impl(h, layer, batch, 1, k_new, v_new, st);
-        if (s != DELTA_OK) return s;
-    }
     cudaError_t e = launch_quest_score(quest_params(h, layer, batch, q), h->L.max_pages, h->sms, st, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "quest score launch");
     ++h->launches;
-    return launch_sel(h, layer, batch, h->at<float>(h->L.keys), nullptr, nullptr, st, 0);
+    return launch_sel(h, layer, batch, h->at<float>(h->L.keys), nullptr, nullptr, st, 0, k_new, v_new);
 }
 
 delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new, const void* v_new,
@@ -515,9 +514,11 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
 }
 
 delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_override, int32_t* idx_out,
-                        int32_t* count_out, cudaStream_t st, int shard_mode) {
+                        int32_t* count_out, cudaStream_t st, int shard_mode, const void* k_new, const void* v_new) {
     const delta_config& c = h->cfg;
     SelectParams p = {};
+    p.k_new = k_new; p.v_new = v_new; p.kv_pool = h->kv_pool; p.reps = h->ws + h->L.reps;
+    p.d = c.head_dim; p.num_phys = c.num_phys_pages;
     const int sl = h->slot[layer];
     p.m = c.num_q_heads; p.g = c.num_kv_heads; p.layer = layer; p.batch = batch;
     p.nchunk = std::max(1, std::min((h->L.max_units + 15) / 16, (2 * h->sms + batch - 1) / batch));

@@ -75,7 +75,7 @@ struct SelectParams {
     int m, g, layer, batch, nchunk;
     int sel_block, n_sink, n_window, k_units;
     int max_batch, max_seq, max_units, plan_cap;
-    const int32_t* seq_len;     // [L][max_batch] raw counters n * g
+    int32_t* seq_len;           // [L][max_batch] raw counters n * g (written by a Quest append)
     const float* logits;        // [max_batch][max_seq][m]
     const float* lse_buf;       // [max_batch][m]
     const float* keys_override; // [batch][ceil(s/sel_block)] or null
@@ -96,6 +96,13 @@ struct SelectParams {
     int shard_mode, page_lo, page_hi;
     uint2* cand_out;            // mode 1: [batch][k_units] (order-preserving key bits, unit)
     int late_trigger;           // 1: launch dependents after the plan is written (else at entry)
+    // Quest layers: this launch also performs the layer's Eq.7 append of one token (pool rows,
+    // page representatives, length counter) before ranking — k_new null otherwise
+    const void* k_new;          // [batch][g][d] bf16
+    const void* v_new;
+    void* kv_pool;              // [L][num_phys][g][2][P][d]
+    void* reps;                 // [L][num_phys][g][2][d]
+    int d, num_phys;
     int hist_mode;              // radix histogram: 0 per-warp private, 1 warp-aggregated shared
     int32_t* plan_lo;           // [max_batch]
     int32_t* plan_hi;

@@ -7,6 +7,8 @@
 //    with the reps of group phi(j) — an upper bound of q_j . k over the page's keys;
 //  * the page plan comes from the unchanged radix top-k (select.cu, keys precomputed) and the
 //    sparse attention kernel reads it (Q3: same forced pages and page budget as DELTA).
+#include <type_traits>
+
 #include "combine.cuh"
 
 namespace delta {
@@ -38,32 +40,74 @@ __global__ void __launch_bounds__(64) quest_reps_kernel(const QuestParams p) {
 }
 
 // Page keys: one warp per page (8 pages per CTA); q of the sequence staged in shared memory as
-// fp32.  Lane l owns the d/32 consecutive elements [l*E, l*E + E); per head the lane's partial
-// sum (ascending e) is reduced over the warp with a fixed xor tree: deterministic.
-template <int D>
+// fp32.  Lane l owns the E = D/32 consecutive elements [l*E, l*E + E).  All G groups' min/max
+// slices of the page are loaded up front (one independent 8- or 4-byte load each), then per
+// head the lane's partial sum (ascending e) is reduced over the warp with a fixed xor tree:
+// deterministic.
+template <int D, int G>
 __global__ void __launch_bounds__(256) quest_score_kernel(const QuestParams p) {
     constexpr int E = D / 32;
+    using Vec = typename std::conditional<E == 4, uint2, uint32_t>::type;  // E bf16
     extern __shared__ float sq[];  // [m][D]
     const int b = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    pdl_wait();
-    pdl_launch_dependents();
+    // Before the dependency wait: the length counter, block table and this layer's reps are not
+    // written by the preceding kernels of a step (only q is), so the first page's reps stream in
+    // while the previous kernel finishes.
     const int n = p.seq_len[p.layer * p.max_batch + b] / p.g;
     const int n_pages = (n + kPage - 1) / kPage;
-    const __nv_bfloat16* q = reinterpret_cast<const __nv_bfloat16*>(p.q) + (size_t)b * p.m * D;
-    for (int i = threadIdx.x; i < p.m * D; i += blockDim.x) sq[i] = __bfloat162float(q[i]);
-    __syncthreads();
     const int gs = p.m / p.g;
-    for (int u = blockIdx.x * 8 + warp; u < n_pages; u += gridDim.x * 8) {
+    auto load_reps = [&](int u, Vec* vmn, Vec* vmx) {
         const int phys = p.block_table[(size_t)b * p.bt_stride + u];
-        const __nv_bfloat16* rep = reinterpret_cast<const __nv_bfloat16*>(p.reps) +
-                                   ((size_t)p.layer * p.num_phys + phys) * p.g * 2 * D;
+        const Vec* rep = reinterpret_cast<const Vec*>(reinterpret_cast<const __nv_bfloat16*>(p.reps) +
+                                                      ((size_t)p.layer * p.num_phys + phys) * p.g * 2 * D);
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            if (h < p.g) {
+                vmn[h] = rep[(size_t)h * 2 * (D / E) + lane];
+                vmx[h] = rep[(size_t)h * 2 * (D / E) + D / E + lane];
+            }
+        }
+    };
+    Vec vmn[G], vmx[G];
+    int u = blockIdx.x * 8 + warp;
+    if (u < n_pages) load_reps(u, vmn, vmx);
+    pdl_wait();
+    pdl_launch_dependents();
+    {   // 16-byte loads of q (all issued before the first store)
+        const uint4* q8 = reinterpret_cast<const uint4*>(p.q) + (size_t)b * p.m * D / 8;
+        constexpr int kPer = 4;
+        for (int i0 = threadIdx.x; i0 < p.m * D / 8; i0 += kPer * blockDim.x) {
+            uint4 x[kPer];
+#pragma unroll
+            for (int r = 0; r < kPer; ++r) {
+                const int i = i0 + r * blockDim.x;
+                if (i < p.m * D / 8) x[r] = q8[i];
+            }
+#pragma unroll
+            for (int r = 0; r < kPer; ++r) {
+                const int i = i0 + r * blockDim.x;
+                if (i < p.m * D / 8) {
+                    const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&x[r]);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) sq[i * 8 + e] = __bfloat162float(hv[e]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (; u < n_pages; u += gridDim.x * 8) {
+        if (u != blockIdx.x * 8 + warp) load_reps(u, vmn, vmx);
         float best = -INFINITY;
-        for (int h = 0; h < p.g; ++h) {
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            if (h >= p.g) break;
             float mn[E], mx[E];
+            const __nv_bfloat16* pn = reinterpret_cast<const __nv_bfloat16*>(&vmn[h]);
+            const __nv_bfloat16* px = reinterpret_cast<const __nv_bfloat16*>(&vmx[h]);
 #pragma unroll
             for (int i = 0; i < E; ++i) {
-                mn[i] = __bfloat162float(rep[(size_t)h * 2 * D + lane * E + i]);
-                mx[i] = __bfloat162float(rep[(size_t)h * 2 * D + D + lane * E + i]);
+                mn[i] = __bfloat162float(pn[i]);
+                mx[i] = __bfloat162float(px[i]);
             }
             for (int jj = 0; jj < gs; ++jj) {
                 const float* qj = sq + (size_t)(h * gs + jj) * D + lane * E;
@@ -106,26 +150,20 @@ cudaError_t launch_quest_score(const QuestParams& p, int max_pages, int sms, cud
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    if (p.d == 128) {
-        static bool set = false;
-        if (!set) {
-            cudaError_t e = cudaFuncSetAttribute(quest_score_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 256 * 128 * 4);
-            if (e != cudaSuccess) return e;
-            set = true;
-        }
-        return cudaLaunchKernelEx(&cfg, quest_score_kernel<128>, p);
+    if (p.g > 16) return cudaErrorInvalidValue;
+    const void* fn = p.d == 128 ? (p.g <= 8 ? (const void*)quest_score_kernel<128, 8> : (const void*)quest_score_kernel<128, 16>)
+                   : p.d == 64  ? (p.g <= 8 ? (const void*)quest_score_kernel<64, 8> : (const void*)quest_score_kernel<64, 16>)
+                                : nullptr;
+    if (!fn) return cudaErrorInvalidValue;
+    static const void* configured[4] = {};
+    const int slot = (p.d == 128 ? 0 : 2) + (p.g <= 8 ? 0 : 1);
+    if (configured[slot] != fn) {  // opt in to > 48 KiB of staged q (m * d fp32, m <= 256)
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 128 * 4);
+        if (e != cudaSuccess) return e;
+        configured[slot] = fn;
     }
-    if (p.d == 64) {
-        static bool set = false;
-        if (!set) {
-            cudaError_t e = cudaFuncSetAttribute(quest_score_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 256 * 64 * 4);
-            if (e != cudaSuccess) return e;
-            set = true;
-        }
-        return cudaLaunchKernelEx(&cfg, quest_score_kernel<64>, p);
-    }
+    void* args[] = {const_cast<QuestParams*>(&p)};
+    return cudaLaunchKernelExC(&cfg, fn, args);
     return cudaErrorInvalidValue;
 }
 

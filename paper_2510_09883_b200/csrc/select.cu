@@ -286,7 +286,46 @@ __global__ void __launch_bounds__(kSelThreads, 2) select_kernel(const SelectPara
     if (!p.late_trigger) pdl_launch_dependents();  // the next kernel's reads of this plan come after its own wait
     if (tid == 0) DTRACE(1);
 
-    const int s = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
+    int s = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
+    if (p.k_new) {
+        // Quest layer: Eq.7 append of this step's token at position s, then
+        // fold it into its page's min/max representatives (quest.cu); a token in slot 0 starts
+        // the page.  One thread per 16-byte chunk of the K and V rows, one per bf16 pair of reps.
+        const int t = s;
+        if (t + 1 > p.max_seq) {
+            if (tid == 0) set_err(p.err, kDevCapacity);
+            return;
+        }
+        const int32_t* btb = p.block_table + (size_t)b * p.bt_stride;
+        const size_t lp = (size_t)p.layer * p.num_phys + btb[t / kPage];
+        const int chunks = p.d / 8;
+        __nv_bfloat16* pool = reinterpret_cast<__nv_bfloat16*>(p.kv_pool);
+        const uint4* kn = reinterpret_cast<const uint4*>(p.k_new) + (size_t)b * p.g * chunks;
+        const uint4* vn = reinterpret_cast<const uint4*>(p.v_new) + (size_t)b * p.g * chunks;
+        for (int i = tid; i < p.g * chunks; i += kSelThreads) {
+            const int hh = i / chunks, c = i - hh * chunks;
+            const size_t row = kv_row(lp, p.g, hh, t % kPage);
+            reinterpret_cast<uint4*>(pool + row * p.d)[c] = kn[i];
+            reinterpret_cast<uint4*>(pool + (row + kPage) * p.d)[c] = vn[i];
+        }
+        const int pairs = p.d / 2;
+        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(p.k_new) + (size_t)b * p.g * pairs;
+        for (int i = tid; i < p.g * pairs; i += kSelThreads) {
+            const int hh = i / pairs, e2 = i - hh * pairs;
+            __nv_bfloat162* rep = reinterpret_cast<__nv_bfloat162*>(p.reps) + (lp * p.g + hh) * p.d;
+            const __nv_bfloat162 k = k2[i];
+            if (t % kPage == 0) {
+                rep[e2] = k;
+                rep[pairs + e2] = k;
+            } else {
+                rep[e2] = __hmin2(rep[e2], k);
+                rep[pairs + e2] = __hmax2(rep[pairs + e2], k);
+            }
+        }
+        __syncthreads();
+        if (tid == 0) p.seq_len[p.layer * p.max_batch + b] = (t + 1) * p.g;
+        s = t + 1;
+    }
     const int block = p.sel_block;
     const int n_units = (s + block - 1) / block;
     float* keys_b = p.keys + (size_t)b * p.max_units;
