@@ -206,6 +206,17 @@ delta_status delta_quest_build_reps(delta_t h, int32_t layer, int32_t batch, cud
 delta_status delta_copy_plan(delta_t h, int32_t layer, int32_t batch, int32_t* idx_out, int32_t* count_out,
                              cudaStream_t stream);
 
+/* Attention recall, Eq.9, a diagnostic (NEXT-2) for a SELECT, SPARSE or
+ * QUEST layer after its decode at this step: R_j = sum_{t in tokens(rho)} alpha_j(t) /
+ * sum_{t < s} alpha_j(t), alpha_j = the layer's exact full-attention weights for its query q
+ * ([batch][m][d] kv_dtype, the same q as the decode), rho = the plan the layer attended (its
+ * own, the governing Delta layer's, or — QUEST — the plan of the latest decoded QUEST layer,
+ * so call it right after that layer).  Runs a full-attention probe of the layer, which
+ * overwrites the Delta-layer logits / LSE buffers: call it after the step's delta_select
+ * calls.  recall_out: device [batch][m] fp32.  Not sequence-sharded. */
+delta_status delta_attention_recall(delta_t h, int32_t layer, int32_t batch, const void* q, float* recall_out,
+                                   cudaStream_t stream);
+
 /* Test hook: device pointers into the workspace.  which = 0: unit keys of the latest selection
  * [max_batch][ceil(max_seq_len/select_block)] fp32; which = 1: Quest page representatives
  * (layout above).  *bytes = size of the region. */

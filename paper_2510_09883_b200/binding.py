@@ -110,6 +110,8 @@ def load_library() -> ctypes.CDLL:
     L.delta_quest_build_reps.restype = st
     L.delta_copy_plan.argtypes = [vp, i32, i32, vp, vp, vp]
     L.delta_copy_plan.restype = st
+    L.delta_attention_recall.argtypes = [vp, i32, i32, vp, vp, vp]
+    L.delta_attention_recall.restype = st
     L.delta_workspace_region.argtypes = [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)]
     L.delta_workspace_region.restype = st
     _lib = L
@@ -282,6 +284,11 @@ class DeltaStack:
     def copy_plan(self, layer: int, batch: int, idx_out, count_out, stream=None):
         _check(self.lib.delta_copy_plan(self.h, layer, batch, _ptr(idx_out), _ptr(count_out), _stream(stream)),
                self.h)
+
+    def attention_recall(self, layer: int, q, recall_out, stream=None):
+        """Eq.9 recall [batch][m] of the plan `layer` attended this step (diagnostic)."""
+        _check(self.lib.delta_attention_recall(self.h, layer, q.shape[0], q.data_ptr(), recall_out.data_ptr(),
+                                               _stream(stream)), self.h)
 
     def workspace_region(self, which: int):
         """(device pointer, bytes) of a workspace region (0 unit keys, 1 Quest reps)."""

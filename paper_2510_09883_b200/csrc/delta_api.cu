@@ -329,12 +329,13 @@ delta_status cuda_fail(delta_ctx* h, cudaError_t e, const char* what) {
     return fail(h, DELTA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-AttnParams attn_params(delta_ctx* h, int layer, int batch) {
+AttnParams attn_params(delta_ctx* h, int layer, int batch, int role_override = -1) {
     const delta_config& c = h->cfg;
     AttnParams p = {};
+    const int hrole = role_override >= 0 ? role_override : h->role[layer];
     p.m = c.num_q_heads; p.g = c.num_kv_heads; p.gs = h->gs; p.d = c.head_dim;
     p.layer = layer; p.batch = batch;
-    p.role = h->role[layer] == kRoleQuest ? kRoleSparse : h->role[layer];  // a Quest layer attends its plan
+    p.role = hrole == kRoleQuest ? kRoleSparse : hrole;  // a Quest layer attends its plan
     p.num_phys = c.num_phys_pages; p.bt_stride = h->L.max_pages;
     p.max_batch = c.max_batch; p.max_seq = c.max_seq_len;
     p.sel_block = c.select_block; p.plan_cap = h->L.plan_cap;
@@ -938,6 +939,45 @@ delta_status delta_copy_plan(delta_t h, int32_t layer, int32_t batch, int32_t* i
                             stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "copy_plan");
     h->last_kind = delta_ctx::kLastNone;  // a copy node sits between kernels
+    return DELTA_OK;
+}
+
+delta_status delta_attention_recall(delta_t h, int32_t layer, int32_t batch, const void* q, float* recall_out,
+                                   cudaStream_t stream) {
+    delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    if (!q || !recall_out) return fail(h, DELTA_ERR_USAGE, "null q/recall_out");
+    if (h->role[layer] == kRoleFull) return fail(h, DELTA_ERR_USAGE, "a FULL layer attends everything (R = 1)");
+    if (h->world > 1) return fail(h, DELTA_ERR_USAGE, "attention recall is not sequence-sharded");
+    const delta_config& c = h->cfg;
+    // 1. full-attention probe of the layer (SELECT role: logits + LSE into the Delta buffers)
+    AttnParams p = attn_params(h, layer, batch, kRoleSelect);
+    p.q = q;
+    p.out = h->at<float>(h->L.stage_out) + (size_t)layer * c.max_batch * c.num_q_heads * c.head_dim;
+    p.lse_out = nullptr;
+    p.fuse_append = 0;
+    p.prewait = 0;
+    p.early_trigger = h->tune_early;
+    cudaError_t e = !h->use_tc ? launch_attn_simt(p, c.kv_dtype == DELTA_BF16, stream, h->pdl)
+                               : launch_attn_tc(p, &h->tm_kv, stream, h->pdl);
+    if (e != cudaSuccess) return cuda_fail(h, e, "recall probe launch");
+    ++h->launches;
+    // 2. Eq.9 over the layer's plan
+    RecallParams rp = {};
+    const int sl = h->slot[h->gov[layer]];
+    rp.m = c.num_q_heads; rp.g = c.num_kv_heads; rp.layer = layer; rp.batch = batch; rp.max_batch = c.max_batch;
+    rp.max_seq = c.max_seq_len; rp.plan_cap = h->L.plan_cap; rp.sel_block = c.select_block;
+    rp.seq_len = h->at<int32_t>(h->L.seq_len);
+    rp.logits = h->at<float>(h->L.logits); rp.lse = h->at<float>(h->L.lse_buf);
+    rp.plan_idx = h->at<int32_t>(h->L.plan_idx) + (size_t)sl * c.max_batch * h->L.plan_cap;
+    rp.plan_count = h->at<int32_t>(h->L.plan_count) + (size_t)sl * c.max_batch;
+    rp.recall_out = recall_out;
+    if (c.num_q_heads > 256) return fail(h, DELTA_ERR_USAGE, "recall supports m <= 256");
+    e = launch_recall(rp, stream, h->pdl);
+    if (e != cudaSuccess) return cuda_fail(h, e, "recall launch");
+    ++h->launches;
+    h->last_kind = delta_ctx::kLastAttn;
+    h->last_layer = layer;
     return DELTA_OK;
 }
 

@@ -146,6 +146,18 @@ struct QuestParams {
 cudaError_t launch_quest_reps(const QuestParams& p, int max_pages, cudaStream_t st, bool pdl);
 cudaError_t launch_quest_score(const QuestParams& p, int max_pages, int sms, cudaStream_t st, bool pdl);
 
+// Attention recall (recall.cu, Eq.9) of one layer's plan against its full-attention probe.
+struct RecallParams {
+    int m, g, layer, batch, max_batch, max_seq, plan_cap, sel_block;
+    const int32_t* seq_len;     // raw counters n * g
+    const float* logits;        // [max_batch][max_seq][m] scaled logits of the probe
+    const float* lse;           // [max_batch][m] natural-log LSE of the probe
+    const int32_t* plan_idx;    // [max_batch][plan_cap] units
+    const int32_t* plan_count;  // [max_batch]
+    float* recall_out;          // [batch][m]
+};
+cudaError_t launch_recall(const RecallParams& p, cudaStream_t st, bool pdl);
+
 // Launchers (attn_tc.cu / attn_simt.cu / select.cu / append.cu).  Each returns the
 // cudaError_t of the launch.  `pdl` enables programmatic dependent launch.
 cudaError_t launch_attn_tc(const AttnParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl);
