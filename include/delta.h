@@ -184,8 +184,13 @@ delta_status delta_decode_step(delta_t h, int32_t batch, const void* q_all, cons
                                cudaStream_t stream);
 
 /* delta_decode_step with HOST buffers (pinned recommended): copies the step's inputs
- * host->device into workspace staging, runs the step, copies out_all device->host, all
- * on `stream`.  Returns after enqueueing; synchronise the stream before reading out. */
+ * host->device into workspace staging, runs the step, copies out_all device->host.
+ * Pipelined: two staging slots and three handle-internal streams (copy-in, compute,
+ * copy-out), so step i's H2D overlaps step i-1's compute and its D2H overlaps step i+1's;
+ * every step still moves its own inputs and outputs.  The first call of a run is ordered
+ * after the work already on `stream`; `stream` waits for each call's D2H, so synchronising
+ * it makes out_all_host valid, and any other call on the handle is ordered after the run.
+ * The host buffers of a call must stay valid until `stream` is synchronised. */
 delta_status delta_decode_step_host(delta_t h, int32_t batch, const void* q_all_host,
                                     const void* k_all_host, const void* v_all_host,
                                     float* out_all_host, cudaStream_t stream);

@@ -188,10 +188,11 @@ Layout layout(const delta_config& c, int sms) {
         L.cand_send = take(L.cand_block);
         L.cand_recv = take(L.cand_block * W);
     }
-    L.stage_q = take((size_t)c.num_layers * c.max_batch * m * D * e);
-    L.stage_k = take((size_t)c.num_layers * c.max_batch * g * D * e);
-    L.stage_v = take((size_t)c.num_layers * c.max_batch * g * D * e);
-    L.stage_out = take((size_t)c.num_layers * c.max_batch * m * D * 4);
+    // host-path staging, two slots (consecutive delta_decode_step_host calls overlap)
+    L.stage_q = take(2 * (size_t)c.num_layers * c.max_batch * m * D * e);
+    L.stage_k = take(2 * (size_t)c.num_layers * c.max_batch * g * D * e);
+    L.stage_v = take(2 * (size_t)c.num_layers * c.max_batch * g * D * e);
+    L.stage_out = take(2 * (size_t)c.num_layers * c.max_batch * m * D * 4);
     L.gslots = std::max(sms, 1) * 2;  // batch * g * nsplit <= sms for every gmerge launch
     L.gpart = take((size_t)L.gslots * gpart_floats(D) * 4);
     L.gcnt = take((size_t)c.max_batch * g * kMaxSplitG * 8);  // ticket counter per (b, h, split count)
@@ -292,10 +293,19 @@ struct delta_ctx {
     float scale = 0.f;
     std::vector<long long> step, dec_step, sel_step;
     // graph cache for delta_decode_step
-    cudaGraphExec_t gexec = nullptr;
-    const void* gkey[7] = {};
-    int gbatch = -1;
-    uint64_t graph_kernels = 0;
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        const void* key[7] = {};
+        int batch = -1;
+        uint64_t kernels = 0;
+    } graphs[3];  // the caller's step + the two host-path staging slots
+    int graph_next = 0;  // round-robin replacement
+    // delta_decode_step_host pipeline: copy-in, compute and copy-out streams, per staging slot
+    // events (inputs landed, step done, outputs read)
+    bool host_init = false, host_pending = false;
+    int host_slot = 0;
+    cudaStream_t hs_in = nullptr, hs_comp = nullptr, hs_out = nullptr;
+    cudaEvent_t hev_in[2] = {}, hev_done[2] = {}, hev_out[2] = {}, hev_join = nullptr;
     uint64_t launches = 0;
     bool pdl = true;
     int tune_nsplit = 0, tune_deep = -1;  // DELTA_TUNE overrides (0 / -1 = automatic)
@@ -327,6 +337,17 @@ delta_status fail(delta_ctx* h, delta_status st, const std::string& m) {
 
 delta_status cuda_fail(delta_ctx* h, cudaError_t e, const char* what) {
     return fail(h, DELTA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Work of earlier delta_decode_step_host calls runs on the handle's internal streams: order the
+// caller's stream after it before any other call enqueues work there.
+delta_status join_host(delta_ctx* h, cudaStream_t st) {
+    if (!h || !h->host_pending) return DELTA_OK;
+    cudaError_t e = cudaEventRecord(h->hev_join, h->hs_comp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, h->hev_join, 0);
+    if (e != cudaSuccess) return cuda_fail(h, e, "join host pipeline");
+    h->host_pending = false;
+    return DELTA_OK;
 }
 
 AttnParams attn_params(delta_ctx* h, int layer, int batch, int role_override = -1) {
@@ -750,7 +771,19 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
 
 delta_status delta_destroy(delta_t h) {
     if (!h) return DELTA_ERR_USAGE;
-    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    for (auto& g : h->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (h->host_init) {
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(h->hev_in[i]);
+            cudaEventDestroy(h->hev_done[i]);
+            cudaEventDestroy(h->hev_out[i]);
+        }
+        cudaEventDestroy(h->hev_join);
+        cudaStreamDestroy(h->hs_in);
+        cudaStreamDestroy(h->hs_comp);
+        cudaStreamDestroy(h->hs_out);
+    }
     if (h->comm) nccl().commDestroy(h->comm);
     delete h;
     return DELTA_OK;
@@ -759,6 +792,7 @@ delta_status delta_destroy(delta_t h) {
 delta_status delta_set_seq_lens(delta_t h, int32_t layer, int32_t batch, const int32_t* lens_host,
                                 cudaStream_t stream) {
     if (!h) return fail(nullptr, DELTA_ERR_USAGE, "null handle");
+    { delta_status j = join_host(h, stream); if (j != DELTA_OK) return j; }
     if (batch < 1 || batch > h->cfg.max_batch || !lens_host) return fail(h, DELTA_ERR_USAGE, "bad batch/lens");
     if (layer < -1 || layer >= h->cfg.num_layers) return fail(h, DELTA_ERR_USAGE, "layer out of range");
     for (int b = 0; b < batch; ++b)
@@ -785,6 +819,8 @@ delta_status delta_append_kv(delta_t h, int32_t layer, int32_t batch, int32_t nt
                              const void* v_new, cudaStream_t stream) {
     delta_status s = check_layer_batch(h, layer, batch);
     if (s != DELTA_OK) return s;
+    s = join_host(h, stream);
+    if (s != DELTA_OK) return s;
     if (ntok < 1 || !k_new || !v_new) return fail(h, DELTA_ERR_USAGE, "bad ntok or null k_new/v_new");
     s = launch_append_impl(h, layer, batch, ntok, k_new, v_new, stream);
     if (s == DELTA_OK) h->step[layer] += 1;
@@ -794,6 +830,8 @@ delta_status delta_append_kv(delta_t h, int32_t layer, int32_t batch, int32_t nt
 delta_status delta_decode_layer(delta_t h, int32_t layer, int32_t batch, const void* q, float* out,
                                 float* lse_out, cudaStream_t stream) {
     delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    s = join_host(h, stream);
     if (s != DELTA_OK) return s;
     if (!q || !out) return fail(h, DELTA_ERR_USAGE, "null q/out");
     s = check_sparse_fresh(h, layer, false);
@@ -807,6 +845,8 @@ delta_status delta_append_decode_layer(delta_t h, int32_t layer, int32_t batch, 
                                        const void* v_new, const void* q, float* out, float* lse_out,
                                        cudaStream_t stream) {
     delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    s = join_host(h, stream);
     if (s != DELTA_OK) return s;
     if (!q || !out || !k_new || !v_new) return fail(h, DELTA_ERR_USAGE, "null pointer");
     s = check_sparse_fresh(h, layer, true);
@@ -822,6 +862,8 @@ delta_status delta_append_decode_layer(delta_t h, int32_t layer, int32_t batch, 
 delta_status delta_select(delta_t h, int32_t layer, int32_t batch, const float* keys_override, int32_t* idx_out,
                           int32_t* count_out, cudaStream_t stream) {
     delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    s = join_host(h, stream);
     if (s != DELTA_OK) return s;
     if (h->role[layer] != kRoleSelect) return fail(h, DELTA_ERR_USAGE, "delta_select on a non-Delta layer");
     if (!keys_override && h->dec_step[layer] != h->step[layer])
@@ -842,6 +884,7 @@ delta_status delta_decode_step(delta_t h, int32_t batch, const void* q_all, cons
         return fail(h, DELTA_ERR_USAGE, "sharded handle without NCCL: drive layers with the delta_shard_* calls");
     if (batch < 1 || batch > h->cfg.max_batch) return fail(h, DELTA_ERR_USAGE, "batch out of range");
     if (!q_all || !k_all || !v_all || !out_all) return fail(h, DELTA_ERR_USAGE, "null pointer");
+    { delta_status j = join_host(h, stream); if (j != DELTA_OK) return j; }
     const bool legacy = (stream == 0 || stream == cudaStreamLegacy || stream == cudaStreamPerThread);
     if (legacy) {  // default streams cannot be captured: run eagerly
         delta_status s = enqueue_step(h, batch, q_all, k_all, v_all, out_all, lse_all, stream);
@@ -849,10 +892,14 @@ delta_status delta_decode_step(delta_t h, int32_t batch, const void* q_all, cons
         return s;
     }
     const void* key[7] = {q_all, k_all, v_all, out_all, lse_all, (const void*)stream, nullptr};
-    bool hit = h->gexec && h->gbatch == batch && std::memcmp(key, h->gkey, sizeof key) == 0;
-    if (!hit) {
-        if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
-        for (int attempt = 0; attempt < 2 && !h->gexec; ++attempt) {
+    delta_ctx::GraphEntry* ge = nullptr;
+    for (auto& g : h->graphs)
+        if (g.exec && g.batch == batch && std::memcmp(key, g.key, sizeof key) == 0) ge = &g;
+    if (!ge) {
+        ge = &h->graphs[h->graph_next];
+        h->graph_next = (h->graph_next + 1) % 3;
+        if (ge->exec) { cudaGraphExecDestroy(ge->exec); ge->exec = nullptr; }
+        for (int attempt = 0; attempt < 2 && !ge->exec; ++attempt) {
             const uint64_t before = h->launches;
             cudaError_t e = cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal);
             if (e != cudaSuccess) return cuda_fail(h, e, "graph capture begin");
@@ -861,47 +908,87 @@ delta_status delta_decode_step(delta_t h, int32_t batch, const void* q_all, cons
             e = cudaStreamEndCapture(stream, &graph);
             if (s != DELTA_OK) { if (graph) cudaGraphDestroy(graph); return s; }
             if (e != cudaSuccess) return cuda_fail(h, e, "graph capture end");
-            h->graph_kernels = h->launches - before;
+            ge->kernels = h->launches - before;
             h->launches = before;
-            e = cudaGraphInstantiate(&h->gexec, graph, 0);
+            e = cudaGraphInstantiate(&ge->exec, graph, 0);
             cudaGraphDestroy(graph);
             if (e != cudaSuccess) {
                 cudaGetLastError();
-                h->gexec = nullptr;
+                ge->exec = nullptr;
                 if (!h->pdl) return cuda_fail(h, e, "graph instantiate");
                 h->pdl = false;  // retry without programmatic edges
             }
         }
-        std::memcpy(h->gkey, key, sizeof key);
-        h->gbatch = batch;
+        std::memcpy(ge->key, key, sizeof key);
+        ge->batch = batch;
     }
-    cudaError_t e = cudaGraphLaunch(h->gexec, stream);
+    cudaError_t e = cudaGraphLaunch(ge->exec, stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "graph launch");
-    h->launches += h->graph_kernels;
+    h->launches += ge->kernels;
     mark_step_done(h);
     return DELTA_OK;
 }
 
+// Host-buffer step, pipelined over two staging slots and three internal streams: step i's
+// H2D (copy-in stream) overlaps step i-1's graph (compute stream), and its D2H (copy-out
+// stream) overlaps step i+1's graph.  Each step still moves its own inputs and outputs.  The
+// caller's stream waits for this step's D2H, so synchronising it makes out_all_host valid.
 delta_status delta_decode_step_host(delta_t h, int32_t batch, const void* q_all_host, const void* k_all_host,
                                     const void* v_all_host, float* out_all_host, cudaStream_t stream) {
     if (!h) return fail(nullptr, DELTA_ERR_USAGE, "null handle");
     if (batch < 1 || batch > h->cfg.max_batch) return fail(h, DELTA_ERR_USAGE, "batch out of range");
     const delta_config& c = h->cfg;
+    cudaError_t err = cudaSuccess;
+    if (!h->host_init) {
+        err = cudaStreamCreateWithFlags(&h->hs_in, cudaStreamNonBlocking);
+        if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&h->hs_comp, cudaStreamNonBlocking);
+        if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&h->hs_out, cudaStreamNonBlocking);
+        for (int i = 0; i < 2 && err == cudaSuccess; ++i) {
+            err = cudaEventCreateWithFlags(&h->hev_in[i], cudaEventDisableTiming);
+            if (err == cudaSuccess) err = cudaEventCreateWithFlags(&h->hev_done[i], cudaEventDisableTiming);
+            if (err == cudaSuccess) err = cudaEventCreateWithFlags(&h->hev_out[i], cudaEventDisableTiming);
+        }
+        if (err == cudaSuccess) err = cudaEventCreateWithFlags(&h->hev_join, cudaEventDisableTiming);
+        if (err != cudaSuccess) return cuda_fail(h, err, "step_host streams");
+        h->host_init = true;
+    }
     const size_t e = elem_bytes(c);
     const size_t qb = (size_t)c.num_layers * batch * c.num_q_heads * c.head_dim * e;
     const size_t kb = (size_t)c.num_layers * batch * c.num_kv_heads * c.head_dim * e;
     const size_t ob = (size_t)c.num_layers * batch * c.num_q_heads * c.head_dim * 4;
-    uint8_t* dq = h->at<uint8_t>(h->L.stage_q);
-    uint8_t* dk = h->at<uint8_t>(h->L.stage_k);
-    uint8_t* dv = h->at<uint8_t>(h->L.stage_v);
-    float* dout = h->at<float>(h->L.stage_out);
-    cudaError_t err = cudaMemcpyAsync(dq, q_all_host, qb, cudaMemcpyHostToDevice, stream);
-    if (err == cudaSuccess) err = cudaMemcpyAsync(dk, k_all_host, kb, cudaMemcpyHostToDevice, stream);
-    if (err == cudaSuccess) err = cudaMemcpyAsync(dv, v_all_host, kb, cudaMemcpyHostToDevice, stream);
+    const size_t qs = (size_t)c.num_layers * c.max_batch * c.num_q_heads * c.head_dim * e;  // slot strides
+    const size_t ks = (size_t)c.num_layers * c.max_batch * c.num_kv_heads * c.head_dim * e;
+    const size_t os = (size_t)c.num_layers * c.max_batch * c.num_q_heads * c.head_dim;
+    const int slot = h->host_slot;
+    h->host_slot ^= 1;
+    uint8_t* dq = h->at<uint8_t>(h->L.stage_q) + slot * qs;
+    uint8_t* dk = h->at<uint8_t>(h->L.stage_k) + slot * ks;
+    uint8_t* dv = h->at<uint8_t>(h->L.stage_v) + slot * ks;
+    float* dout = h->at<float>(h->L.stage_out) + slot * os;
+    if (!h->host_pending) {  // first of a run of host steps: after the caller's prior work
+        err = cudaEventRecord(h->hev_out[slot ^ 1], stream);
+        if (err == cudaSuccess) err = cudaStreamWaitEvent(h->hs_in, h->hev_out[slot ^ 1], 0);
+        if (err == cudaSuccess) err = cudaStreamWaitEvent(h->hs_comp, h->hev_out[slot ^ 1], 0);
+        if (err != cudaSuccess) return cuda_fail(h, err, "step_host join");
+    }
+    // copy-in: the slot is free once step i-2's graph and D2H are done with it
+    err = cudaStreamWaitEvent(h->hs_in, h->hev_done[slot], 0);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(h->hs_in, h->hev_out[slot], 0);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(dq, q_all_host, qb, cudaMemcpyHostToDevice, h->hs_in);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(dk, k_all_host, kb, cudaMemcpyHostToDevice, h->hs_in);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(dv, v_all_host, kb, cudaMemcpyHostToDevice, h->hs_in);
+    if (err == cudaSuccess) err = cudaEventRecord(h->hev_in[slot], h->hs_in);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(h->hs_comp, h->hev_in[slot], 0);
     if (err != cudaSuccess) return cuda_fail(h, err, "step_host H2D");
-    delta_status s = delta_decode_step(h, batch, dq, dk, dv, dout, nullptr, stream);
+    h->host_pending = false;  // the compute stream is ordered after everything above
+    delta_status s = delta_decode_step(h, batch, dq, dk, dv, dout, nullptr, h->hs_comp);
     if (s != DELTA_OK) return s;
-    err = cudaMemcpyAsync(out_all_host, dout, ob, cudaMemcpyDeviceToHost, stream);
+    h->host_pending = true;
+    err = cudaEventRecord(h->hev_done[slot], h->hs_comp);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(h->hs_out, h->hev_done[slot], 0);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(out_all_host, dout, ob, cudaMemcpyDeviceToHost, h->hs_out);
+    if (err == cudaSuccess) err = cudaEventRecord(h->hev_out[slot], h->hs_out);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(stream, h->hev_out[slot], 0);
     if (err != cudaSuccess) return cuda_fail(h, err, "step_host D2H");
     return DELTA_OK;
 }
@@ -909,6 +996,7 @@ delta_status delta_decode_step_host(delta_t h, int32_t batch, const void* q_all_
 delta_status delta_quest_build_reps(delta_t h, int32_t layer, int32_t batch, cudaStream_t stream) {
     if (!h) return fail(nullptr, DELTA_ERR_USAGE, "null handle");
     if (h->cfg.policy != DELTA_POLICY_QUEST) return fail(h, DELTA_ERR_USAGE, "not a QUEST handle");
+    { delta_status j = join_host(h, stream); if (j != DELTA_OK) return j; }
     if (batch < 1 || batch > h->cfg.max_batch) return fail(h, DELTA_ERR_USAGE, "batch out of range");
     if (layer < -1 || layer >= h->cfg.num_layers) return fail(h, DELTA_ERR_USAGE, "layer out of range");
     const int l0 = layer < 0 ? 0 : layer, l1 = layer < 0 ? h->cfg.num_layers : layer + 1;
@@ -926,6 +1014,8 @@ delta_status delta_quest_build_reps(delta_t h, int32_t layer, int32_t batch, cud
 delta_status delta_copy_plan(delta_t h, int32_t layer, int32_t batch, int32_t* idx_out, int32_t* count_out,
                              cudaStream_t stream) {
     delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    s = join_host(h, stream);
     if (s != DELTA_OK) return s;
     if (h->role[layer] == kRoleFull) return fail(h, DELTA_ERR_USAGE, "a FULL layer has no plan");
     const int sl = h->slot[h->gov[layer]];
@@ -945,6 +1035,8 @@ delta_status delta_copy_plan(delta_t h, int32_t layer, int32_t batch, int32_t* i
 delta_status delta_attention_recall(delta_t h, int32_t layer, int32_t batch, const void* q, float* recall_out,
                                    cudaStream_t stream) {
     delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    s = join_host(h, stream);
     if (s != DELTA_OK) return s;
     if (!q || !recall_out) return fail(h, DELTA_ERR_USAGE, "null q/recall_out");
     if (h->role[layer] == kRoleFull) return fail(h, DELTA_ERR_USAGE, "a FULL layer attends everything (R = 1)");
@@ -996,6 +1088,7 @@ delta_status delta_workspace_region(delta_t h, int32_t which, void** ptr, size_t
 }
 
 delta_status delta_get_error(delta_t h, cudaStream_t stream, delta_status* sticky) {
+    { delta_status j = join_host(h, stream); if (j != DELTA_OK) return j; }
     if (!h || !sticky) return fail(h, DELTA_ERR_USAGE, "null argument");
     cudaError_t e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "get_error sync");
@@ -1062,6 +1155,8 @@ delta_status delta_shard_merge(delta_t h, int32_t layer, int32_t batch, float* o
                                cudaStream_t stream) {
     delta_status s = check_layer_batch(h, layer, batch);
     if (s != DELTA_OK) return s;
+    s = join_host(h, stream);
+    if (s != DELTA_OK) return s;
     if (h->world < 2 || h->comm) return fail(h, DELTA_ERR_USAGE, "delta_shard_merge needs a sharded handle without NCCL");
     if (!out) return fail(h, DELTA_ERR_USAGE, "null out");
     return launch_merge(h, layer, batch, out, lse_out, stream);
@@ -1070,6 +1165,8 @@ delta_status delta_shard_merge(delta_t h, int32_t layer, int32_t batch, float* o
 delta_status delta_shard_select_merge(delta_t h, int32_t layer, int32_t batch, int32_t* idx_out,
                                       int32_t* count_out, cudaStream_t stream) {
     delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    s = join_host(h, stream);
     if (s != DELTA_OK) return s;
     if (h->world < 2 || h->comm) return fail(h, DELTA_ERR_USAGE, "delta_shard_select_merge needs a sharded handle without NCCL");
     if (h->role[layer] != kRoleSelect) return fail(h, DELTA_ERR_USAGE, "not a Delta layer");

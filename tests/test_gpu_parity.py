@@ -193,6 +193,33 @@ def test_step_host_buffers_equal_device():
     np.testing.assert_array_equal(out_a, out_h.numpy())
 
 
+def test_step_host_pipelined_multi_step():
+    """Consecutive delta_decode_step_host calls overlap (two staging slots, internal streams):
+    every step's host output equals the device-buffer step's, bitwise, and a per-layer call
+    after the run is ordered after it."""
+    a = GpuCase(BF16_SMALL, 24, batch=2, s_pre=1499, max_seq=1600)
+    b = GpuCase(BF16_SMALL, 24, batch=2, s_pre=1499, max_seq=1600)
+    st = torch.cuda.Stream()
+    outs_h = []
+    ref = []
+    for s in range(1500, 1505):
+        out_a, _ = a.step_graph(s)
+        ref.append(out_a)
+        q, k, v = b.inputs(s)
+        qh, kh, vh = q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()
+        out_h = torch.empty(out_a.shape, dtype=torch.float32).pin_memory()
+        b.stack.decode_step_host(qh, kh, vh, out_h, stream=st)
+        outs_h.append((out_h, qh, kh, vh))      # keep the pinned inputs alive until the sync
+    st.synchronize()
+    for r, (oh, *_) in zip(ref, outs_h):
+        np.testing.assert_array_equal(r, oh.numpy())
+    # a device-buffer step after the host run continues the same cache
+    out_a, _ = a.step_graph(1505)
+    out_b, _ = b.step_graph(1505)
+    np.testing.assert_array_equal(out_a, out_b)
+    assert b.stack.get_error() == 0
+
+
 def test_deterministic_across_runs():
     outs = []
     for _ in range(2):
