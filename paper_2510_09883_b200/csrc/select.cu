@@ -140,17 +140,29 @@ __device__ __forceinline__ int topk_regs(const SelectParams& p, int n_units, int
     const int ipt = IPT;
     const int u0 = tid * ipt;
     uint32_t key[IPT];
-    int32_t* s_phys = reinterpret_cast<int32_t*>(sm_keys);  // unused key cache: >= n_units slots
-    uint32_t cand = 0, live = 0;
+    // coalesced staging (unit u = i * kSelThreads + tid) of the keys' order-preserving bits and
+    // the units' physical locations into shared memory, then contiguous ownership for the scan
+    uint32_t* s_key = sm_keys;                                                  // [n_units]
+    int32_t* s_phys = reinterpret_cast<int32_t*>(sm_keys + n_units);            // [n_units]
     bool bad = false;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        const int u = i * kSelThreads + tid;
+        if (u < n_units) {
+            const float f = __ldcg(src + u);
+            s_key[u] = key_bits(f);
+            s_phys[u] = phys_of(u);
+            bad |= isnan(f);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) DTRACE(11);
+    uint32_t cand = 0, live = 0;
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
         const int u = u0 + i;
         const bool in = i < ipt && u < n_units;
-        const float f = in ? __ldcg(src + u) : 0.f;
-        if (in) s_phys[u] = phys_of(u);
-        key[i] = key_bits(f);
-        bad |= in && isnan(f);
+        key[i] = in ? s_key[u] : 0u;
         if (in) live |= 1u << i;
         if (in && !forced(u)) cand |= 1u << i;
     }
@@ -377,14 +389,19 @@ __global__ void __launch_bounds__(kSelThreads, 2) select_kernel(const SelectPara
                 if (t < t_hi && hh == 0) keys_b[t] = mx;
             }
         }
-        __threadfence();
+        // arrival: the barrier puts every thread's key stores before thread 0's acq_rel atomic
+        // (release, cumulative); the last arrival's acquire + the barrier order its threads'
+        // key loads after every other CTA's stores — no per-thread fences
         __syncthreads();
         if (tid == 0) DTRACE(2);
-        if (tid == 0) s_flag = (atomicAdd(&p.cnt[b], 1) == p.nchunk - 1);
+        if (tid == 0) {
+            int old;
+            asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.cnt + b) : "memory");
+            s_flag = (old == p.nchunk - 1);
+        }
         __syncthreads();
         if (!s_flag) return;
         if (tid == 0) DTRACE(3);
-        __threadfence();
         if (tid == 0) p.cnt[b] = 0;
     }
 
@@ -662,7 +679,8 @@ extern "C" int delta_trace_read_select(void* host, size_t bytes) {  // this TU's
 #endif
 
 size_t select_smem_bytes(int max_units) {
-    return (size_t)min(max_units, kSmemUnits) * sizeof(uint32_t);
+    // keys (and, on the register path, the units' physical locations: 2 x 4 B per unit)
+    return (size_t)min(max_units, kSmemUnits) * sizeof(uint32_t) * 2;
 }
 
 cudaError_t launch_select(const SelectParams& p, cudaStream_t st, bool pdl) {
@@ -670,7 +688,7 @@ cudaError_t launch_select(const SelectParams& p, cudaStream_t st, bool pdl) {
     static bool configured = false;  // static + dynamic shared memory exceeds the 48 KiB default
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)select_smem_bytes(kSmemUnits));
+                                             (int)(2 * kSmemUnits * sizeof(uint32_t)));
         if (e != cudaSuccess) return e;
         configured = true;
     }

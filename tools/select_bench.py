@@ -29,7 +29,7 @@ def timeit(fn, s, reps=200):
 
 
 def main():
-    ctx = 32768
+    ctx = int(os.environ.get("SEL_CTX", "32768"))
     L, m, g, d, F, delta = 32, 32, 8, 128, 2, [2, 16, 25]
     cfg = d200.DeltaConfig(num_layers=L, num_q_heads=m, num_kv_heads=g, head_dim=d, max_batch=1,
                            max_seq_len=ctx + 64, num_full_prefix=F, select_layers=delta, budget_k=2048,

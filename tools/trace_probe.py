@@ -88,7 +88,7 @@ def report(name, tr3):
 
 
 def main():
-    ctx = 32768
+    ctx = int(os.environ.get("PROBE_CTX", "32768"))
     L, m, g, d, F, delta = 32, 32, 8, 128, 2, [2, 16, 25]
     cfg = d200.DeltaConfig(num_layers=L, num_q_heads=m, num_kv_heads=g, head_dim=d, max_batch=1,
                            max_seq_len=ctx + 64, num_full_prefix=F, select_layers=delta, budget_k=2048,
@@ -181,7 +181,7 @@ def main():
                     print(f"   select L{l - 32}: entry {g(0, np.min):7.2f} waited {g(1, np.max):7.2f} phaseA_done "
                           f"{g(2, np.max):7.2f} elected {g(3, np.max):7.2f} radix_done {g(4, np.max):7.2f} "
                           f"plan_done {g(5, np.max):7.2f} | keys {g(6, np.max):7.2f} passes {g(7, np.max):7.2f} "
-                          f"{g(8, np.max):7.2f} {g(9, np.max):7.2f} {g(10, np.max):7.2f}")
+                          f"{g(8, np.max):7.2f} {g(9, np.max):7.2f} {g(10, np.max):7.2f} | staged {g(11, np.max):7.2f}")
                 continue
             t = tr[l]
             live = t[:, 0] > 0
