@@ -471,6 +471,11 @@ def run_ours(args, c):
                      "kernel": "attn_tc_kernel<128,false> FULL, one layer, s=%d" % s_last,
                      "algorithmic_bytes_per_launch": kbytes, "avg_launch_us": round(us_kernel, 3),
                      "peak_source": peak_src},
+        # the SPARSE-layer kernel (27 of 32 layers at C1; the larger share of the DELTA step's time at b = 1)
+        "roofline_sparse": {"bound": "hbm", "achieved": round(sp_bytes / (us_sparse * 1e-6) / 1e9, 1), "peak": peak,
+                            "unit": "GB/s", "frac": round(sp_bytes / (us_sparse * 1e-6) / 1e9 / peak, 4),
+                            "kernel": "attn_tc_kernel<128,false> SPARSE (cluster split-K), one layer",
+                            "algorithmic_bytes_per_launch": sp_bytes, "avg_launch_us": round(us_sparse, 3)},
         "kernels": kernels,
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": round(ms_e2e / K, 5)},
