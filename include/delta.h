@@ -222,6 +222,15 @@ delta_status delta_copy_plan(delta_t h, int32_t layer, int32_t batch, int32_t* i
 delta_status delta_attention_recall(delta_t h, int32_t layer, int32_t batch, const void* q, float* recall_out,
                                    cudaStream_t stream);
 
+/* Chunked prefill (NEXT-3; the step before the decode path, PAPER.md:34-45 over a prompt,
+ * SPEC.md:387-395): appends ntok tokens per sequence (Eq.7, as delta_append_kv; Quest reps
+ * too), then for each new token i at position n_b + i computes Eq.4 over tokens t <= n_b + i
+ * (causal), every head j against group phi(j).  q: device [batch][ntok][m][d] bf16; k_new,
+ * v_new: [batch][ntok][g][d] bf16; out: [batch][ntok][m][d] fp32; lse_out: optional
+ * [batch][ntok][m] fp32.  bf16 KV only; not sequence-sharded.  Two launches. */
+delta_status delta_prefill(delta_t h, int32_t layer, int32_t batch, int32_t ntok, const void* q, const void* k_new,
+                           const void* v_new, float* out, float* lse_out, cudaStream_t stream);
+
 /* Test hook: device pointers into the workspace.  which = 0: unit keys of the latest selection
  * [max_batch][ceil(max_seq_len/select_block)] fp32; which = 1: Quest page representatives
  * (layout above).  *bytes = size of the region. */

@@ -112,6 +112,8 @@ def load_library() -> ctypes.CDLL:
     L.delta_copy_plan.restype = st
     L.delta_attention_recall.argtypes = [vp, i32, i32, vp, vp, vp]
     L.delta_attention_recall.restype = st
+    L.delta_prefill.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]
+    L.delta_prefill.restype = st
     L.delta_workspace_region.argtypes = [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)]
     L.delta_workspace_region.restype = st
     _lib = L
@@ -289,6 +291,11 @@ class DeltaStack:
         """Eq.9 recall [batch][m] of the plan `layer` attended this step (diagnostic)."""
         _check(self.lib.delta_attention_recall(self.h, layer, q.shape[0], q.data_ptr(), recall_out.data_ptr(),
                                                _stream(stream)), self.h)
+
+    def prefill(self, layer: int, q, k_new, v_new, out, lse=None, stream=None):
+        """Chunked prefill: append q.shape[1] tokens and attend causally (q [B][ntok][m][d])."""
+        _check(self.lib.delta_prefill(self.h, layer, q.shape[0], q.shape[1], q.data_ptr(), k_new.data_ptr(),
+                                      v_new.data_ptr(), out.data_ptr(), _ptr(lse), _stream(stream)), self.h)
 
     def workspace_region(self, which: int):
         """(device pointer, bytes) of a workspace region (0 unit keys, 1 Quest reps)."""

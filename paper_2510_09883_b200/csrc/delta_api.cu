@@ -1073,6 +1073,33 @@ delta_status delta_attention_recall(delta_t h, int32_t layer, int32_t batch, con
     return DELTA_OK;
 }
 
+delta_status delta_prefill(delta_t h, int32_t layer, int32_t batch, int32_t ntok, const void* q, const void* k_new,
+                           const void* v_new, float* out, float* lse_out, cudaStream_t stream) {
+    delta_status s = check_layer_batch(h, layer, batch);
+    if (s != DELTA_OK) return s;
+    s = join_host(h, stream);
+    if (s != DELTA_OK) return s;
+    if (ntok < 1 || !q || !k_new || !v_new || !out) return fail(h, DELTA_ERR_USAGE, "bad ntok or null pointer");
+    if (!h->use_tc) return fail(h, DELTA_ERR_USAGE, "prefill needs bf16 KV");
+    if (h->world > 1) return fail(h, DELTA_ERR_USAGE, "prefill is not sequence-sharded");
+    const delta_config& c = h->cfg;
+    s = launch_append_impl(h, layer, batch, ntok, k_new, v_new, stream);  // Eq.7 for the chunk (+ Quest reps)
+    if (s != DELTA_OK) return s;
+    PrefillParams p = {};
+    p.m = c.num_q_heads; p.g = c.num_kv_heads; p.gs = h->gs; p.d = c.head_dim; p.layer = layer; p.batch = batch;
+    p.ntok = ntok; p.num_phys = c.num_phys_pages; p.bt_stride = h->L.max_pages; p.max_batch = c.max_batch;
+    p.scale_log2 = (float)((double)h->scale * 1.4426950408889634);
+    p.q = q; p.kv_pool = h->kv_pool; p.block_table = h->block_table; p.seq_len = h->at<int32_t>(h->L.seq_len);
+    p.out = out; p.lse_out = lse_out; p.err = h->at<int32_t>(h->L.err);
+    cudaError_t e = launch_prefill(p, stream, h->pdl);
+    if (e != cudaSuccess) return cuda_fail(h, e, "prefill launch");
+    ++h->launches;
+    h->last_kind = delta_ctx::kLastAttn;
+    h->last_layer = layer;
+    h->step[layer] += 1;
+    return DELTA_OK;
+}
+
 delta_status delta_workspace_region(delta_t h, int32_t which, void** ptr, size_t* bytes) {
     if (!h || !ptr || !bytes) return fail(h, DELTA_ERR_USAGE, "null argument");
     if (which == 0) {

@@ -158,6 +158,21 @@ struct RecallParams {
 };
 cudaError_t launch_recall(const RecallParams& p, cudaStream_t st, bool pdl);
 
+// Chunked prefill (prefill.cu): causal attention of ntok appended tokens per sequence.
+struct PrefillParams {
+    int m, g, gs, d, layer, batch, ntok, num_phys, bt_stride, max_batch;
+    float scale_log2;
+    const void* q;              // [batch][ntok][m][d] bf16
+    const void* kv_pool;
+    const int32_t* block_table;
+    const int32_t* seq_len;     // raw counters n * g, AFTER the chunk's append
+    float* out;                 // [batch][ntok][m][d]
+    float* lse_out;             // [batch][ntok][m] or null
+    int32_t* err;
+};
+cudaError_t launch_prefill(const PrefillParams& p, cudaStream_t st, bool pdl);
+size_t prefill_smem_bytes(int d, int gs);
+
 // Launchers (attn_tc.cu / attn_simt.cu / select.cu / append.cu).  Each returns the
 // cudaError_t of the launch.  `pdl` enables programmatic dependent launch.
 cudaError_t launch_attn_tc(const AttnParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl);
