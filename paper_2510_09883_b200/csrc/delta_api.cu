@@ -29,7 +29,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
     size_t seq_len, err, cnt_sel, logits, lse_buf, keys, plan_idx, plan_phys, plan_count, plan_stamp, plan_lo, plan_hi,
-        shard_send, shard_recv, cand_send, cand_recv, stage_q, stage_k, stage_v, stage_out, gpart, gcnt, reps,
+        shard_send, shard_recv, cand_send, cand_recv, stage_q, stage_k, stage_v, stage_out, gpart, gcnt, reps, ticket,
         reps_bytes, total;
     int gslots;  // split partial slots of the global-merge kernels
     size_t shard_block, cand_block;  // bytes of one rank's attention partial / candidate block
@@ -169,6 +169,7 @@ Layout layout(const delta_config& c, int sms) {
     L.seq_len = take((size_t)c.num_layers * c.max_batch * 4);
     L.err = take(16);
     L.cnt_sel = take((size_t)c.num_layers * c.max_batch * 4);
+    L.ticket = take((size_t)c.num_layers * c.max_batch * 4);
     L.logits = take(has_sel ? (size_t)c.max_batch * c.max_seq_len * m * 4 : 0);
     L.lse_buf = take((size_t)c.max_batch * m * 4);
     L.keys = take(has_sel ? (size_t)c.max_batch * L.max_units * 4 : 0);
@@ -469,6 +470,7 @@ delta_status launch_append_impl(delta_ctx* h, int layer, int batch, int ntok, co
     p.max_seq = h->cfg.max_seq_len; p.elem_bytes = elem_bytes(h->cfg);
     p.k_new = k_new; p.v_new = v_new; p.kv_pool = h->kv_pool;
     p.reps = h->role[layer] == kRoleQuest ? h->ws + h->L.reps : nullptr;
+    p.ticket = h->at<int32_t>(h->L.ticket);
     p.block_table = h->block_table; p.seq_len = h->at<int32_t>(h->L.seq_len); p.err = h->at<int32_t>(h->L.err);
     p.page_lo = h->page_lo; p.page_hi = h->page_hi;
     cudaError_t e = launch_append(p, st, h->pdl);

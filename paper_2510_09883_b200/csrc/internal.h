@@ -124,6 +124,7 @@ struct ShardMergeParams {
 struct AppendParams {
     int g, d, layer, batch, ntok, num_phys, bt_stride, max_batch, max_seq, elem_bytes;
     void* reps;         // Quest layers: [L][num_phys][g][2][d] bf16 page min/max, updated per token
+    int32_t* ticket;    // [L][max_batch] arrival tickets of multi-CTA appends (reset by the last)
     int page_lo, page_hi;  // sequence sharding: this rank writes rows on its pages only
     const void* k_new;  // [batch][ntok][g][d]
     const void* v_new;

@@ -4,8 +4,9 @@
 // Query i of the chunk sits at position pos_i = n0 + i and attends tokens t <= pos_i (Eq.4 with
 // the causal mask), GQA head j reads group phi(j) = j / gs (R15).
 //
-// CTA = (block of QB = 16 query tokens, kv head h, sequence b); its rows are the QB x gs
-// (token, head) pairs of the group, 16 rows per warp (gs warps).  The CTA streams the head's
+// CTA = (block of QB = 32 (gs <= 8) or 16 query tokens, kv head h, sequence b), latest blocks
+// (longest causal rows) first; its rows are the QB x gs (token, head) pairs of the group, 16
+// rows per warp.  The CTA streams the head's
 // K|V pages (the decode kernels' 8 KiB (page, head) tile, 128-byte swizzle) through a
 // double-buffered cp.async ring; per page and warp: S = Q K^T (m16n8k16, bf16 -> fp32,
 // 2 token tiles x d/16), causal mask, online softmax in the exp2 domain, O += P V with P as
@@ -16,13 +17,14 @@
 namespace delta {
 namespace {
 
-constexpr int kQB = 16;  // query tokens per CTA
+// query tokens per CTA: QB x gs rows, 16 per warp (QB = 32 for gs <= 8, else 16: <= 16 warps)
+__host__ __device__ constexpr int prefill_qb(int gs) { return gs <= 8 ? 32 : 16; }
 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int D>
+template <int D, int kQB>
 __global__ void __launch_bounds__(512) prefill_kernel(const PrefillParams p) {
     constexpr int QS = D + 8;                     // padded Q row (bf16): conflict-free ldmatrix
     constexpr int kTile = TileLayout<D>::kBytes;  // K rows then V rows of one (page, head)
@@ -31,7 +33,7 @@ __global__ void __launch_bounds__(512) prefill_kernel(const PrefillParams p) {
     uint8_t* ring = base;                                                   // [2][kTile]
     __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(base + 2 * kTile);  // [rows][QS]
 
-    const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;  // longest rows first
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nthr = blockDim.x;
     const int g4 = lane >> 2, t4 = lane & 3;
     const int gs = p.gs, rows = kQB * gs;
@@ -213,13 +215,14 @@ __global__ void __launch_bounds__(512) prefill_kernel(const PrefillParams p) {
 
 size_t prefill_smem_bytes(int d, int gs) {
     return 1024 + 2 * (size_t)(d == 128 ? TileLayout<128>::kBytes : TileLayout<64>::kBytes) +
-           (size_t)kQB * gs * (d + 8) * 2;
+           (size_t)prefill_qb(gs) * gs * (d + 8) * 2;
 }
 
 cudaError_t launch_prefill(const PrefillParams& p, cudaStream_t st, bool pdl) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((p.ntok + kQB - 1) / kQB, p.g, p.batch);
-    cfg.blockDim = dim3(32 * p.gs);
+    const int qb = prefill_qb(p.gs);
+    cfg.gridDim = dim3((p.ntok + qb - 1) / qb, p.g, p.batch);
+    cfg.blockDim = dim3(32 * p.gs * qb / 16);
     cfg.dynamicSmemBytes = prefill_smem_bytes(p.d, p.gs);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -227,13 +230,16 @@ cudaError_t launch_prefill(const PrefillParams& p, cudaStream_t st, bool pdl) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    const void* fn = p.d == 128 ? (const void*)prefill_kernel<128> : p.d == 64 ? (const void*)prefill_kernel<64> : nullptr;
+    const bool big = qb == 32;
+    const void* fn = p.d == 128 ? (big ? (const void*)prefill_kernel<128, 32> : (const void*)prefill_kernel<128, 16>)
+                   : p.d == 64  ? (big ? (const void*)prefill_kernel<64, 32> : (const void*)prefill_kernel<64, 16>)
+                                : nullptr;
     if (!fn) return cudaErrorInvalidValue;
-    static const void* configured[2] = {};
-    const int slot = p.d == 128 ? 0 : 1;
+    static const void* configured[4] = {};
+    const int slot = (p.d == 128 ? 0 : 2) + (big ? 1 : 0);
     if (configured[slot] != fn) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)prefill_smem_bytes(128, kMaxGs));
+                                             (int)std::max(prefill_smem_bytes(128, 8), prefill_smem_bytes(128, kMaxGs)));
         if (e != cudaSuccess) return e;
         configured[slot] = fn;
     }
