@@ -8,7 +8,7 @@
 // (longest causal rows) first; its rows are the QB x gs (token, head) pairs of the group, 16
 // rows per warp.  The CTA streams the head's
 // K|V pages (the decode kernels' 8 KiB (page, head) tile, 128-byte swizzle) through a
-// double-buffered cp.async ring; per page and warp: S = Q K^T (m16n8k16, bf16 -> fp32,
+// double-buffered cp.async ring of two-page stages; per page and warp: S = Q K^T (m16n8k16, bf16 -> fp32,
 // 2 token tiles x d/16), causal mask, online softmax in the exp2 domain, O += P V with P as
 // bf16 hi + lo (two MMAs, ~16-bit probabilities as in the decode kernels, R18).
 // Tensor cores on a dense contraction: mma.sync here; the tcgen05 version is the next step.
@@ -19,6 +19,7 @@ namespace {
 
 // query tokens per CTA: QB x gs rows, 16 per warp (QB = 32 for gs <= 8, else 16: <= 16 warps)
 __host__ __device__ constexpr int prefill_qb(int gs) { return gs <= 8 ? 32 : 16; }
+constexpr int kPPS = 2;  // pages per ring stage (32 tokens between barriers)
 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -30,8 +31,8 @@ __global__ void __launch_bounds__(512) prefill_kernel(const PrefillParams p) {
     constexpr int kTile = TileLayout<D>::kBytes;  // K rows then V rows of one (page, head)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* ring = base;                                                   // [2][kTile]
-    __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(base + 2 * kTile);  // [rows][QS]
+    uint8_t* ring = base;                                                         // [2][kPPS][kTile]
+    __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(base + 2 * kPPS * kTile);  // [rows][QS]
 
     const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;  // longest rows first
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nthr = blockDim.x;
@@ -62,9 +63,9 @@ __global__ void __launch_bounds__(512) prefill_kernel(const PrefillParams p) {
                 *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
         }
     }
-    auto load_page = [&](int u, int buf) {
+    auto load_page = [&](int u, int slot) {
         const size_t row0 = kv_row(layer_ph + bt[u], p.g, h, 0);  // 2P contiguous rows: K then V
-        uint8_t* dst = ring + buf * kTile;
+        uint8_t* dst = ring + slot * kTile;
         constexpr int C = D / 8;
         for (int x = tid; x < 2 * kPage * C; x += nthr) {
             const int r = x / C, c = x - r * C;  // r < P: K row r; r >= P: V row r - P
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(512) prefill_kernel(const PrefillParams p) {
             cp_async16(d, src);
         }
     };
-    load_page(0, 0);
+    for (int k = 0; k < kPPS && k < npages; ++k) load_page(k, k);
     cp_async_commit();
 
     // this warp's 16 rows: row g4 and g4 + 8 of the tile; their query positions
@@ -89,12 +90,14 @@ __global__ void __launch_bounds__(512) prefill_kernel(const PrefillParams p) {
     uint32_t qa[D / 16][4];
     bool q_loaded = false;
 
-    for (int u = 0; u < npages; ++u) {
-        const int buf = u & 1;
-        if (u + 1 < npages) load_page(u + 1, buf ^ 1);
+    for (int u0 = 0; u0 < npages; u0 += kPPS) {
+        const int buf = (u0 / kPPS) & 1;
+        for (int k = 0; k < kPPS && u0 + kPPS + k < npages; ++k) load_page(u0 + kPPS + k, (buf ^ 1) * kPPS + k);
         cp_async_commit();
-        cp_async_wait<1>();  // page u (and Q) landed
+        cp_async_wait<1>();  // this stage's pages (and Q) landed
         __syncthreads();
+        for (int sub = 0; sub < kPPS && u0 + sub < npages; ++sub) {
+        const int u = u0 + sub;
         if (live_w) {
             if (!q_loaded) {
                 const uint32_t qbase = smem_u32(sq + (size_t)(warp * 16) * QS);
@@ -104,7 +107,7 @@ __global__ void __launch_bounds__(512) prefill_kernel(const PrefillParams p) {
                             qa[kc][1], qa[kc][2], qa[kc][3]);
                 q_loaded = true;
             }
-            const uint32_t kt = smem_u32(ring + buf * kTile), vt = kt + TileLayout<D>::kVOff;
+            const uint32_t kt = smem_u32(ring + (buf * kPPS + sub) * kTile), vt = kt + TileLayout<D>::kVOff;
             // S[16 rows x 16 tokens] = Q K^T: token tile nt = tokens 8nt..8nt+7
             float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
@@ -180,6 +183,7 @@ __global__ void __launch_bounds__(512) prefill_kernel(const PrefillParams p) {
                 mma_bf16_16816(o[2 * dp + 1], pa_l, v2, v3);
             }
         }
+        }
         __syncthreads();  // buffer buf is refilled by the next iteration's prefetch
     }
     if (!live_w) return;
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(512) prefill_kernel(const PrefillParams p) {
 }  // namespace
 
 size_t prefill_smem_bytes(int d, int gs) {
-    return 1024 + 2 * (size_t)(d == 128 ? TileLayout<128>::kBytes : TileLayout<64>::kBytes) +
+    return 1024 + 2 * kPPS * (size_t)(d == 128 ? TileLayout<128>::kBytes : TileLayout<64>::kBytes) +
            (size_t)prefill_qb(gs) * gs * (d + 8) * 2;
 }
 
