@@ -71,6 +71,9 @@ def lib():
         L.oracle_attention_recall.restype = c_dbl
         L.oracle_quest_reps.argtypes = [ctypes.c_void_p, c_i64, P(c_dbl)]
         L.oracle_quest_scores.argtypes = [P(ctypes.c_float), c_i32, c_i32, c_i32, P(c_dbl), c_i64, P(c_dbl)]
+        L.oracle_raas_step.argtypes = [c_i64, P(c_dbl), c_i64, c_dbl, P(ctypes.c_char), c_i64, P(ctypes.c_char),
+                                       P(c_i64), P(c_i64)]
+        L.oracle_raas_step.restype = c_i64
         L.oracle_page_of.argtypes = [c_i64, c_i32]
         L.oracle_page_of.restype = c_i64
         L.oracle_append.argtypes = [
@@ -264,6 +267,59 @@ def quest_scores(q, reps) -> np.ndarray:
     _check(lib().oracle_quest_scores(_ptr(q, ctypes.c_float), m, g, d, _ptr(reps, ctypes.c_double), n_pages,
                                      _ptr(out, ctypes.c_double)), "quest_scores")
     return out
+
+
+def raas_step(S, step: int, threshold: float, exempt, capacity: int, retained, last):
+    """One RaaS refresh + eviction (readings RS1-RS4).  `retained` (uint8) and
+    `last` (int64) are updated in place; returns the evicted pages in eviction order."""
+    S = np.ascontiguousarray(S, dtype=np.float64)
+    ex = np.ascontiguousarray(exempt, dtype=np.uint8)
+    assert retained.dtype == np.uint8 and last.dtype == np.int64 and retained.flags.c_contiguous
+    out = np.empty(S.size, np.int64)
+    n = lib().oracle_raas_step(S.size, _ptr(S, ctypes.c_double), step, threshold, _ptr(ex, ctypes.c_char), capacity,
+                               _ptr(retained, ctypes.c_char), _ptr(last, ctypes.c_int64), _ptr(out, ctypes.c_int64))
+    assert n >= 0
+    return out[:n].copy()
+
+
+def raas_exempt(n_pages: int, s: int, P: int, n_sink: int, n_window: int) -> np.ndarray:
+    """RS4: sink pages (overlapping [0, S)) and recency pages (overlapping [s - L, s))."""
+    ex = np.zeros(n_pages, np.uint8)
+    if n_sink > 0 and s > 0:
+        ex[: (min(n_sink, s) - 1) // P + 1] = 1
+    if n_window > 0:
+        ex[max(0, s - n_window) // P:] = 1
+    return ex
+
+
+def raas_layer_step(cfg: "StackConfig", kv: SeqKV, q, s: int, retained, last, scores_override=None):
+    """One RaaS layer at cache length s (RS1-RS4): the new token's page joins the retained set,
+    attention over tokens(retained) (softmax renormalised over them), page scores
+    S_u = sum_{t in u} max_j alpha_j(t) over the attended tokens, threshold P / |attended|,
+    refresh + eviction of the non-exempt pages beyond k/P.  `retained` / `last` are per page
+    arrays with room for ceil(s/P) pages, updated in place.  `scores_override` replaces the
+    page scores (to replay a GPU run's fp32 scores).  Returns (out, lse, attended_pages, S, evicted)."""
+    P = cfg.page_size
+    n_pages = -(-s // P)
+    if (s - 1) % P == 0:                       # the appended token opened a page: created now
+        retained[(s - 1) // P] = 1
+        last[(s - 1) // P] = s
+    pages = np.nonzero(retained[:n_pages])[0]
+    tokens = units_to_tokens(pages, P, s)
+    out, lse, alpha = decode_heads(q, kv, tokens, cfg.scale, want_alpha=True)
+    s_t = token_scores(alpha)                  # max over heads of the renormalised weights (R7)
+    S = np.zeros(n_pages, np.float64)
+    for t, v in zip(tokens, s_t):
+        S[t // P] += v
+    if scores_override is not None:
+        S = np.where(retained[:n_pages] > 0, scores_override[:n_pages], 0.0)
+    ex = raas_exempt(n_pages, s, P, cfg.n_sink, cfg.n_window)
+    ret = np.ascontiguousarray(retained[:n_pages])
+    lst = np.ascontiguousarray(last[:n_pages])
+    ev = raas_step(S, s, P / tokens.size, ex, cfg.budget_k // P, ret, lst)
+    retained[:n_pages] = ret
+    last[:n_pages] = lst
+    return out, lse, pages, S, ev
 
 
 def quest_layer(cfg: "StackConfig", kv: SeqKV, q, s: int, nthreads=0):

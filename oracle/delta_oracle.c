@@ -310,3 +310,28 @@ int oracle_quest_scores(const float* q, int32_t m, int32_t g, int32_t d,
     }
     return ORACLE_OK;
 }
+
+/* ---------------------------------------------------------------- RaaS (NEXT-4) */
+
+int64_t oracle_raas_step(int64_t n_pages, const double* S, int64_t current_step, double threshold,
+                         const char* exempt, int64_t capacity, char* retained, int64_t* last,
+                         int64_t* evicted_out) {
+    if (n_pages < 0 || capacity < 0) return -1;
+    /* 1. refresh: "pages with S_u >= threshold get last_salient_step := current_step" */
+    for (int64_t u = 0; u < n_pages; ++u)
+        if (retained[u] && S[u] >= threshold) last[u] = current_step;
+    /* 2. evict the least recently salient non-exempt pages until `capacity` remain */
+    int64_t n_evicted = 0;
+    for (;;) {
+        int64_t count = 0, victim = -1;
+        for (int64_t u = 0; u < n_pages; ++u) {
+            if (!retained[u] || exempt[u]) continue;
+            ++count;
+            if (victim < 0 || last[u] < last[victim]) victim = u; /* ties: lowest index (scan order) */
+        }
+        if (count <= capacity) break;
+        retained[victim] = 0;
+        evicted_out[n_evicted++] = victim;
+    }
+    return n_evicted;
+}

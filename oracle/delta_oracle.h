@@ -151,6 +151,21 @@ int oracle_quest_reps(const oracle_seq_kv* kv, int64_t s, double* reps);
 int oracle_quest_scores(const float* q, int32_t m, int32_t g, int32_t d,
                         const double* reps, int64_t n_pages, double* out);
 
+/* ---------------------------------------------------------------- RaaS (NEXT-4)
+ * The paper's eviction baseline RaaS ("an eviction-based method that removes
+ * pages with consistently low attention scores ... risking the loss of tokens that may later
+ * become important").  Readings RS1-RS4: one step of the
+ * threshold-refresh / least-recently-salient rule for ONE (layer, sequence):
+ *   1. retained pages u with S[u] >= threshold get last[u] = current_step;
+ *   2. while more than `capacity` retained pages are not exempt: evict the non-exempt retained
+ *      page with the smallest (last[u], u) — retained[u] = 0 for good.
+ * S: [n_pages] scores (entries of non-retained pages ignored); exempt, retained: [n_pages]
+ * 0/1; last: [n_pages].  evicted_out receives the evicted pages in eviction order; returns
+ * their number. */
+int64_t oracle_raas_step(int64_t n_pages, const double* S, int64_t current_step, double threshold,
+                         const char* exempt, int64_t capacity, char* retained, int64_t* last,
+                         int64_t* evicted_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -461,3 +461,63 @@ def test_quest_dominant_page_selected_and_budget_all():
     units = oracle.select(keys, s, P, 4, 32, 1)                      # sink page 0 + 2 window pages + 1
     assert units.tolist() == [0, 5, 10, 11]
     assert oracle.select(keys, s, P, 4, 32, 9).tolist() == list(range(12))
+
+
+# ---------------------------------------------------------------- RaaS (NEXT-4)
+
+def _raas(S, step, thr, exempt, cap, retained, last):
+    r = np.array(retained, np.uint8)
+    l = np.array(last, np.int64)
+    ev = oracle.raas_step(np.array(S, float), step, thr, np.array(exempt, np.uint8), cap, r, l)
+    return ev.tolist(), r.tolist(), l.tolist()
+
+
+def test_raas_capacity_covers_all_no_eviction():
+    """capacity >= page count -> no eviction; salient pages are refreshed."""
+    ev, r, l = _raas([0.5, 0.1, 0.9, 0.0], 7, 0.25, [0, 0, 0, 0], 4, [1, 1, 1, 1], [0, 0, 0, 0])
+    assert ev == [] and r == [1, 1, 1, 1] and l == [7, 0, 7, 0]
+
+
+def test_raas_never_salient_evicted_before_refreshed():
+    """a page that never reaches the threshold goes before any refreshed page,
+    whatever their indices."""
+    ev, r, _ = _raas([0.9, 0.9, 0.0, 0.9], 3, 0.5, [0, 0, 0, 0], 3, [1, 1, 1, 1], [1, 1, 1, 1])
+    assert ev == [2] and r == [1, 1, 0, 1]
+
+
+def test_raas_scripted_five_pages_capacity_three():
+    """a scripted score sequence over 5 pages, capacity 3, page 4 exempt (recency).
+    Hand simulation of the rule (refresh at >= 0.3, evict smallest (last, index)):
+      step 1: S = [.5 .0 .4 .1 .9]: last = [1 0 1 0 0] ; non-exempt {0,1,2,3} > 3 -> evict 1
+      step 2: S = [.0 - .6 .5 .9]:  last = [1 - 2 2 0] ; {0,2,3} = 3 -> none
+      step 3: S = [.4 - .0 .0 .9]:  last = [3 - 2 2 0] ; none
+      step 4: cap 2 (budget shrinks): {0,2,3}: lasts 3,2,2 -> evict 2 (tie 2,2: lowest index)"""
+    retained = np.ones(5, np.uint8)
+    last = np.zeros(5, np.int64)
+    ex = np.array([0, 0, 0, 0, 1], np.uint8)
+    evs = []
+    for step, S, cap in [(1, [.5, .0, .4, .1, .9], 3), (2, [.0, .0, .6, .5, .9], 3), (3, [.4, .0, .0, .0, .9], 3),
+                         (4, [.0, .0, .0, .0, .9], 2)]:
+        evs.append(oracle.raas_step(np.array(S), step, 0.3, ex, cap, retained, last).tolist())
+    assert evs == [[1], [], [], [2]]
+    assert retained.tolist() == [1, 0, 0, 1, 1]
+    assert last.tolist() == [3, 0, 2, 2, 4]
+
+
+def test_raas_invariants_random():
+    """retained non-exempt count never exceeds capacity, exempt pages are never
+    evicted, evicted pages never come back (200 random steps)."""
+    rng = np.random.default_rng(9)
+    n, cap = 40, 6
+    retained = np.ones(n, np.uint8)
+    last = np.zeros(n, np.int64)
+    gone = set()
+    for step in range(1, 201):
+        ex = (rng.random(n) < 0.1).astype(np.uint8)
+        ex[-3:] = 1
+        before = retained.copy()
+        ev = oracle.raas_step(rng.random(n), step, 0.7, ex, cap, retained, last)
+        assert all(before[u] and not ex[u] for u in ev)
+        assert int(((retained > 0) & (ex == 0)).sum()) <= cap
+        gone |= set(ev.tolist())
+        assert not any(retained[u] for u in gone)
