@@ -252,15 +252,15 @@ def run_ours(args, c):
     max_seq = s_first + K + PAGE
     seed = 2511 if seq_shard else 2511 + 1000 * rank  # batch sharding: every rank its own sequences
 
-    def make_cfg(full: bool, quest: bool = False):
+    def make_cfg(full: bool, quest: bool = False, raas: bool = False):
         return d200.DeltaConfig(num_layers=c["L"], num_q_heads=c["m"], num_kv_heads=c["g"], head_dim=c["d"],
                                 max_batch=batch, max_seq_len=max_seq,
                                 num_full_prefix=c["L"] if full else c["F"],
-                                select_layers=[] if (full or quest) else c["delta"],
+                                select_layers=[] if (full or quest or raas) else c["delta"],
                                 budget_k=c["k"], n_sink=S_SINK, n_window=L_WIN, select_block=PAGE,
                                 shard_world=world if seq_shard else 1, shard_rank=rank if seq_shard else 0,
                                 nccl_id=nccl_ids[1 if full else 0],
-                                policy=d200.POLICY_QUEST if quest else d200.POLICY_DELTA)
+                                policy=(d200.POLICY_QUEST if quest else d200.POLICY_RAAS if raas else d200.POLICY_DELTA))
 
     cfg = make_cfg(False)
     bt = torch.from_numpy(synth.block_table(seed, batch, cfg.max_pages))
@@ -278,6 +278,13 @@ def run_ours(args, c):
         _, qws = d200.query_sizes(qcfg)
         quest = d200.DeltaStack(qcfg, delta.kv_pool, delta.block_table,
                                 torch.zeros(qws, dtype=torch.uint8, device=dev))
+    # the paper's eviction baseline RaaS (NEXT-4) on the same pools (its own retained sets)
+    raas = None
+    if not seq_shard:
+        rcfg = make_cfg(False, raas=True)
+        _, rws = d200.query_sizes(rcfg)
+        raas = d200.DeltaStack(rcfg, delta.kv_pool, delta.block_table,
+                               torch.zeros(rws, dtype=torch.uint8, device=dev))
     t0 = time.time()
     sd.fill_pools(delta.kv_pool, delta.block_table, seed, s_pre, batch, range(c["L"]))
     if quest is not None:
@@ -305,6 +312,8 @@ def run_ours(args, c):
 
     def time_stack(stack, clocks=None):
         stack.set_seq_lens([s_pre] * batch)
+        if stack is raas:
+            stack.raas_reset(-1, batch, stream=stream)  # every page retained; warm-up steps evict to the budget
         with torch.cuda.stream(stream):
             for i in range(W):
                 stack.decode_step(q_all[i], k_all[i], v_all[i], out, stream=stream)
@@ -331,6 +340,11 @@ def run_ours(args, c):
     ms_delta, launches, clk = time_stack(delta, clocks)
     ms_full, _, _ = time_stack(full)
     ms_quest = time_stack(quest)[0] if quest is not None else None
+    ms_raas = time_stack(raas)[0] if raas is not None else None
+    for other in (quest, raas):
+        if other is not None:
+            e_other = other.get_error()
+            assert e_other == 0, f"device error flag {e_other} (comparison stack)"
     err = delta.get_error()
     assert err == 0, f"device error flag {err}"
 
@@ -346,6 +360,8 @@ def run_ours(args, c):
     ms_full = max_over_ranks(ms_full)
     if ms_quest is not None:
         ms_quest = max_over_ranks(ms_quest)
+    if ms_raas is not None:
+        ms_raas = max_over_ranks(ms_raas)
 
     # algorithmic bytes over the timed steps (s grows by one per step)
     byts_delta = byts_full = 0
@@ -433,6 +449,7 @@ def run_ours(args, c):
     if rank == 0:
         log(f"DELTA {1e3 * ms_delta / K:.1f} us/step, Full {1e3 * ms_full / K:.1f} us/step, "
             f"speedup {ms_full / ms_delta:.3f}x; Quest {1e3 * ms_quest / K if ms_quest else 0:.1f} us/step; "
+            f"RaaS {1e3 * ms_raas / K if ms_raas else 0:.1f} us/step; "
             f"kernels {kernels}")
 
     if rank != 0:
@@ -463,6 +480,7 @@ def run_ours(args, c):
         "speedup_vs_full": round(ms_full / ms_delta, 3),
         "quest_stack_us": round(1e3 * ms_quest / K, 2) if ms_quest else None,
         "quest_speedup_vs_full": round(ms_full / ms_quest, 3) if ms_quest else None,
+        "raas_stack_us": round(1e3 * ms_raas / K, 2) if ms_raas else None,
         "byte_ratio": round(byte_ratio, 3),
         "speedup_target": round(0.8 * byte_ratio, 3),
         "full_stack_gbs": round(byts_full * (1 if seq_shard else world) / (ms_full * 1e-3) / 1e9, 2),

@@ -49,7 +49,8 @@ typedef enum {
 
 typedef enum { DELTA_BF16 = 0, DELTA_FP32 = 1 } delta_dtype;
 
-typedef enum { DELTA_ROLE_FULL = 0, DELTA_ROLE_SELECT = 1, DELTA_ROLE_SPARSE = 2, DELTA_ROLE_QUEST = 3 } delta_role;
+typedef enum { DELTA_ROLE_FULL = 0, DELTA_ROLE_SELECT = 1, DELTA_ROLE_SPARSE = 2, DELTA_ROLE_QUEST = 3,
+               DELTA_ROLE_RAAS = 4 } delta_role;
 
 /* Selection policy of the layers >= F.
  *  DELTA: the paper's three-tier schedule (Delta layers select, sparse layers reuse).
@@ -59,7 +60,14 @@ typedef enum { DELTA_ROLE_FULL = 0, DELTA_ROLE_SELECT = 1, DELTA_ROLE_SPARSE = 2
  *         an upper bound of q_j . k over the page), selects the forced sink/window pages plus the
  *         top budget_k/P candidate pages with the same rule as DELTA (Q3) and attends to them.
  *         Needs num_select_layers == 0, select_block == page_size, kv_dtype BF16, shard_world 1. */
-typedef enum { DELTA_POLICY_DELTA = 0, DELTA_POLICY_QUEST = 1 } delta_policy;
+/*  RAAS:  the paper's eviction baseline RaaS (readings RS1-RS4):
+ *         every layer >= F (role RAAS) attends its own retained page set, then scores the
+ *         retained pages with its attention weights (S_u = sum_{t in u} max_j alpha_j(t)),
+ *         refreshes pages with S_u >= P / |attended tokens|, and permanently evicts the least
+ *         recently salient non-exempt pages beyond budget_k/P (sink and recency pages exempt).
+ *         Same restrictions as QUEST.  delta_raas_reset starts every sequence with all pages
+ *         retained. */
+typedef enum { DELTA_POLICY_DELTA = 0, DELTA_POLICY_QUEST = 1, DELTA_POLICY_RAAS = 2 } delta_policy;
 
 /* Problem statement of the method (PAPER.md:157-158 schedule, 168-171/185 budget and
  * window, 180-181/196 paged layout). */
@@ -205,6 +213,11 @@ delta_status delta_decode_step_host(delta_t h, int32_t batch, const void* q_all_
  * page keys, top-k (select.cu), sparse attention over the plan — four launches. */
 delta_status delta_quest_build_reps(delta_t h, int32_t layer, int32_t batch, cudaStream_t stream);
 
+/* RaaS policy: (re)start the retained sets of sequences [0, batch) of one RAAS layer (or all,
+ * layer == -1) at their current length n: every page < ceil(n/P) retained with last-salient
+ * step 0 (plus the page of position n if n is page-aligned).  Call after filling the cache. */
+delta_status delta_raas_reset(delta_t h, int32_t layer, int32_t batch, cudaStream_t stream);
+
 /* Test hook: device copy of the plan that `layer` attends (a Delta layer's plan, the plan of
  * the governing Delta layer of a SPARSE layer, or a QUEST layer's own plan from its latest
  * decode): idx_out [batch][plan_capacity] (entries past count unspecified), count_out [batch]. */
@@ -232,8 +245,9 @@ delta_status delta_prefill(delta_t h, int32_t layer, int32_t batch, int32_t ntok
                            const void* v_new, float* out, float* lse_out, cudaStream_t stream);
 
 /* Test hook: device pointers into the workspace.  which = 0: unit keys of the latest selection
- * [max_batch][ceil(max_seq_len/select_block)] fp32; which = 1: Quest page representatives
- * (layout above).  *bytes = size of the region. */
+ * [max_batch][ceil(max_seq_len/select_block)] fp32 (RAAS: the page scores of the latest RAAS
+ * layer's update, by page); which = 1: Quest page representatives (layout above); which = 2:
+ * RaaS last-salient steps [L][max_batch][ceil(max_seq_len/P)] int32.  *bytes = region size. */
 delta_status delta_workspace_region(delta_t h, int32_t which, void** ptr, size_t* bytes);
 
 /* Synchronises `stream`, reads and clears the sticky device error flag.

@@ -292,7 +292,8 @@ def raas_exempt(n_pages: int, s: int, P: int, n_sink: int, n_window: int) -> np.
     return ex
 
 
-def raas_layer_step(cfg: "StackConfig", kv: SeqKV, q, s: int, retained, last, scores_override=None):
+def raas_layer_step(cfg: "StackConfig", kv: SeqKV, q, s: int, retained, last, scores_override=None,
+                    threshold=None):
     """One RaaS layer at cache length s (RS1-RS4): the new token's page joins the retained set,
     attention over tokens(retained) (softmax renormalised over them), page scores
     S_u = sum_{t in u} max_j alpha_j(t) over the attended tokens, threshold P / |attended|,
@@ -316,7 +317,8 @@ def raas_layer_step(cfg: "StackConfig", kv: SeqKV, q, s: int, retained, last, sc
     ex = raas_exempt(n_pages, s, P, cfg.n_sink, cfg.n_window)
     ret = np.ascontiguousarray(retained[:n_pages])
     lst = np.ascontiguousarray(last[:n_pages])
-    ev = raas_step(S, s, P / tokens.size, ex, cfg.budget_k // P, ret, lst)
+    ev = raas_step(S, s, P / tokens.size if threshold is None else threshold(tokens.size), ex, cfg.budget_k // P,
+                   ret, lst)
     retained[:n_pages] = ret
     last[:n_pages] = lst
     return out, lse, pages, S, ev

@@ -3,11 +3,12 @@
 The product is ``libdelta.so`` (C ABI in ``include/delta.h``; sm_100a kernels in
 ``csrc/``); :mod:`.binding` is a thin ctypes layer over it.
 """
-from .binding import (DELTA_BF16, DELTA_FP32, POLICY_DELTA, POLICY_QUEST, ROLE_FULL, ROLE_QUEST, ROLE_SELECT,
-                      ROLE_SPARSE, DeltaConfig, DeltaError,
+from .binding import (DELTA_BF16, DELTA_FP32, POLICY_DELTA, POLICY_QUEST, POLICY_RAAS, ROLE_FULL, ROLE_QUEST,
+                      ROLE_RAAS, ROLE_SELECT, ROLE_SPARSE, DeltaConfig, DeltaError,
                       DeltaStack, declared_functions, load_library, nccl_unique_id, query_sizes, shard_range)
 
-__all__ = ["DELTA_BF16", "DELTA_FP32", "POLICY_DELTA", "POLICY_QUEST", "ROLE_FULL", "ROLE_QUEST", "ROLE_SELECT",
+__all__ = ["DELTA_BF16", "DELTA_FP32", "POLICY_DELTA", "POLICY_QUEST", "POLICY_RAAS", "ROLE_FULL", "ROLE_QUEST",
+           "ROLE_RAAS", "ROLE_SELECT",
            "ROLE_SPARSE", "DeltaConfig", "DeltaError",
            "DeltaStack", "declared_functions", "load_library", "nccl_unique_id", "query_sizes",
            "shard_range"]

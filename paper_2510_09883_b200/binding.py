@@ -18,8 +18,8 @@ LIB_PATH = os.environ.get("DELTA_LIB_PATH") or os.path.join(_HERE, "libdelta.so"
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "delta.h")
 
 DELTA_BF16, DELTA_FP32 = 0, 1
-ROLE_FULL, ROLE_SELECT, ROLE_SPARSE, ROLE_QUEST = 0, 1, 2, 3
-POLICY_DELTA, POLICY_QUEST = 0, 1
+ROLE_FULL, ROLE_SELECT, ROLE_SPARSE, ROLE_QUEST, ROLE_RAAS = 0, 1, 2, 3, 4
+POLICY_DELTA, POLICY_QUEST, POLICY_RAAS = 0, 1, 2
 STATUS = {0: "OK", 1: "CONFIG", 2: "USAGE", 3: "NUMERIC", 4: "CAPACITY", 5: "CUDA", 6: "NCCL"}
 
 
@@ -112,6 +112,8 @@ def load_library() -> ctypes.CDLL:
     L.delta_copy_plan.restype = st
     L.delta_attention_recall.argtypes = [vp, i32, i32, vp, vp, vp]
     L.delta_attention_recall.restype = st
+    L.delta_raas_reset.argtypes = [vp, i32, i32, vp]
+    L.delta_raas_reset.restype = st
     L.delta_prefill.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]
     L.delta_prefill.restype = st
     L.delta_workspace_region.argtypes = [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)]
@@ -282,6 +284,9 @@ class DeltaStack:
 
     def quest_build_reps(self, layer: int = -1, batch: int | None = None, stream=None):
         _check(self.lib.delta_quest_build_reps(self.h, layer, batch or self.cfg.max_batch, _stream(stream)), self.h)
+
+    def raas_reset(self, layer: int = -1, batch: int | None = None, stream=None):
+        _check(self.lib.delta_raas_reset(self.h, layer, batch or self.cfg.max_batch, _stream(stream)), self.h)
 
     def copy_plan(self, layer: int, batch: int, idx_out, count_out, stream=None):
         _check(self.lib.delta_copy_plan(self.h, layer, batch, _ptr(idx_out), _ptr(count_out), _stream(stream)),

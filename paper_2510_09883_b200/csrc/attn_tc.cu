@@ -362,7 +362,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
 #pragma unroll
                     for (int i = 0; i < 4; ++i) c[i] = acc[nh][i] + acc2[nh][i];
                     // c[0],c[1]: token tok0, heads 2t4, 2t4+1; c[2],c[3]: token tok1
-                    if (p.role == kRoleSelect) {
+                    if (p.emit_logits) {
                         float* lg = p.logits + (size_t)b * p.max_seq * p.m + h * gs;
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {

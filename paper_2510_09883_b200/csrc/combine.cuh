@@ -251,7 +251,7 @@ __device__ __forceinline__ void cluster_epilogue(const AttnParams& p, const floa
                         p.part_lse[(size_t)b * p.m + j] = lse;
                     } else {
                         if (p.lse_out) p.lse_out[(size_t)b * p.m + j] = lse;
-                        if (p.role == kRoleSelect) p.lse_buf[(size_t)b * p.m + j] = lse;
+                        if (p.emit_logits) p.lse_buf[(size_t)b * p.m + j] = lse;
                     }
                 }
             }
@@ -332,7 +332,7 @@ __device__ __forceinline__ void global_epilogue(const AttnParams& p, const float
                 p.part_lse[(size_t)b * p.m + j] = lse;
             } else {
                 if (p.lse_out) p.lse_out[(size_t)b * p.m + j] = lse;
-                if (p.role == kRoleSelect) p.lse_buf[(size_t)b * p.m + j] = lse;
+                if (p.emit_logits) p.lse_buf[(size_t)b * p.m + j] = lse;
             }
         }
     };

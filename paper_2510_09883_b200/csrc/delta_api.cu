@@ -30,6 +30,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 struct Layout {
     size_t seq_len, err, cnt_sel, logits, lse_buf, keys, plan_idx, plan_phys, plan_count, plan_stamp, plan_lo, plan_hi,
         shard_send, shard_recv, cand_send, cand_recv, stage_q, stage_k, stage_v, stage_out, gpart, gcnt, reps, ticket,
+        raas_last,
         reps_bytes, total;
     int gslots;  // split partial slots of the global-merge kernels
     size_t shard_block, cand_block;  // bytes of one rank's attention partial / candidate block
@@ -107,14 +108,15 @@ std::string validate(const delta_config& c, std::vector<int>& role, std::vector<
     if (c.shard_world < 1 || c.shard_world > 64 || c.shard_rank < 0 || c.shard_rank >= c.shard_world)
         return "shard_world must be in [1, 64] and 0 <= shard_rank < shard_world";
     if (c.softmax_scale < 0.f || !std::isfinite(c.softmax_scale)) return "softmax_scale must be finite and >= 0";
-    if (c.policy != DELTA_POLICY_DELTA && c.policy != DELTA_POLICY_QUEST) return "policy must be DELTA or QUEST";
-    if (c.policy == DELTA_POLICY_QUEST) {
-        // Quest: every layer >= F selects its own pages (readings Q1-Q3)
-        if (c.num_select_layers != 0) return "QUEST policy takes no Delta layers";
-        if (c.select_block != c.page_size) return "QUEST selects pages: select_block must be page_size";
-        if (c.kv_dtype != DELTA_BF16) return "QUEST needs bf16 KV";
-        if (c.shard_world != 1) return "QUEST is not sequence-sharded";
-        role.assign(c.num_layers, kRoleQuest);
+    if (c.policy != DELTA_POLICY_DELTA && c.policy != DELTA_POLICY_QUEST && c.policy != DELTA_POLICY_RAAS)
+        return "policy must be DELTA, QUEST or RAAS";
+    if (c.policy != DELTA_POLICY_DELTA) {
+        // Quest / RaaS: every layer >= F selects (Q1-Q3) or evicts (RS1-RS4) its own pages
+        if (c.num_select_layers != 0) return "QUEST / RAAS policies take no Delta layers";
+        if (c.select_block != c.page_size) return "QUEST / RAAS work on pages: select_block must be page_size";
+        if (c.kv_dtype != DELTA_BF16) return "QUEST / RAAS need bf16 KV";
+        if (c.shard_world != 1) return "QUEST / RAAS are not sequence-sharded";
+        role.assign(c.num_layers, c.policy == DELTA_POLICY_QUEST ? kRoleQuest : kRoleRaas);
         gov.assign(c.num_layers, 0);
         for (int l = 0; l < c.num_layers; ++l) {
             if (l < c.num_full_prefix) role[l] = kRoleFull;
@@ -162,18 +164,21 @@ Layout layout(const delta_config& c, int sms) {
         const int sink_units = c.n_sink > 0 ? (c.n_sink + blk - 1) / blk : 0;
         const int win_units = c.n_window > 0 ? (blk == 1 ? c.n_window : (c.n_window - 1) / blk + 2) : 0;
         L.plan_cap = std::max(1, std::min(L.max_units, k_units + sink_units + win_units));
+        if (c.policy == DELTA_POLICY_RAAS) L.plan_cap = L.max_pages + 1;  // starts with every page retained
     }
-    const bool has_sel = c.num_select_layers > 0 || c.policy == DELTA_POLICY_QUEST;  // keys + plan
+    const bool has_sel = c.num_select_layers > 0 || c.policy != DELTA_POLICY_DELTA;  // logits, keys, plans
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + std::max<size_t>(bytes, 1)); return o; };
     L.seq_len = take((size_t)c.num_layers * c.max_batch * 4);
     L.err = take(16);
     L.cnt_sel = take((size_t)c.num_layers * c.max_batch * 4);
     L.ticket = take((size_t)c.num_layers * c.max_batch * 4);
+    L.raas_last = take(c.policy == DELTA_POLICY_RAAS ? (size_t)c.num_layers * c.max_batch * L.max_pages * 4 : 0);
     L.logits = take(has_sel ? (size_t)c.max_batch * c.max_seq_len * m * 4 : 0);
     L.lse_buf = take((size_t)c.max_batch * m * 4);
     L.keys = take(has_sel ? (size_t)c.max_batch * L.max_units * 4 : 0);
-    const int nd = std::max(1, L.n_delta);  // (QUEST: n_delta = 0, slot 0 = the current layer's plan)
+    // plan slots: one per Delta layer; QUEST: slot 0 = the current layer's plan; RAAS: one per layer
+    const int nd = c.policy == DELTA_POLICY_RAAS ? c.num_layers : std::max(1, L.n_delta);
     L.plan_idx = take((size_t)nd * c.max_batch * L.plan_cap * 4);
     L.plan_phys = take((size_t)nd * c.max_batch * L.plan_cap * 4);
     L.plan_count = take((size_t)nd * c.max_batch * 4);
@@ -357,7 +362,8 @@ AttnParams attn_params(delta_ctx* h, int layer, int batch, int role_override = -
     const int hrole = role_override >= 0 ? role_override : h->role[layer];
     p.m = c.num_q_heads; p.g = c.num_kv_heads; p.gs = h->gs; p.d = c.head_dim;
     p.layer = layer; p.batch = batch;
-    p.role = hrole == kRoleQuest ? kRoleSparse : hrole;  // a Quest layer attends its plan
+    p.role = (hrole == kRoleQuest || hrole == kRoleRaas) ? kRoleSparse : hrole;  // they attend their plan
+    p.emit_logits = (hrole == kRoleSelect || hrole == kRoleRaas) ? 1 : 0;
     p.num_phys = c.num_phys_pages; p.bt_stride = h->L.max_pages;
     p.max_batch = c.max_batch; p.max_seq = c.max_seq_len;
     p.sel_block = c.select_block; p.plan_cap = h->L.plan_cap;
@@ -496,6 +502,26 @@ delta_status launch_quest_select(delta_ctx* h, int layer, int batch, const void*
     return launch_sel(h, layer, batch, h->at<float>(h->L.keys), nullptr, nullptr, st, 0, k_new, v_new);
 }
 
+RaasParams raas_params(delta_ctx* h, int layer, int batch) {
+    const delta_config& c = h->cfg;
+    RaasParams p = {};
+    const int sl = h->slot[layer];
+    p.m = c.num_q_heads; p.g = c.num_kv_heads; p.layer = layer; p.batch = batch; p.max_batch = c.max_batch;
+    p.max_seq = c.max_seq_len; p.max_pages = h->L.max_pages; p.plan_cap = h->L.plan_cap;
+    p.n_sink = c.n_sink; p.n_window = c.n_window; p.k_pages = c.budget_k / c.page_size;
+    p.seq_len = h->at<int32_t>(h->L.seq_len);
+    p.logits = h->at<float>(h->L.logits); p.lse = h->at<float>(h->L.lse_buf);
+    p.plan_idx = h->at<int32_t>(h->L.plan_idx) + (size_t)sl * c.max_batch * h->L.plan_cap;
+    p.plan_phys = h->at<int32_t>(h->L.plan_phys) + (size_t)sl * c.max_batch * h->L.plan_cap;
+    p.plan_count = h->at<int32_t>(h->L.plan_count) + (size_t)sl * c.max_batch;
+    p.plan_stamp = h->at<int32_t>(h->L.plan_stamp) + (size_t)sl * c.max_batch;
+    p.last = h->at<int32_t>(h->L.raas_last) + (size_t)layer * c.max_batch * h->L.max_pages;
+    p.scores = h->at<float>(h->L.keys); p.max_units = h->L.max_units;
+    p.block_table = h->block_table; p.bt_stride = h->L.max_pages;
+    p.ticket = h->at<int32_t>(h->L.ticket);
+    return p;
+}
+
 delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new, const void* v_new,
                            const void* q, float* out, float* lse_out, cudaStream_t st, bool in_step = false) {
     if (h->role[layer] == kRoleQuest) {
@@ -529,6 +555,11 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
     ++h->launches;
     h->last_kind = delta_ctx::kLastAttn;
     h->last_layer = layer;
+    if (h->role[layer] == kRoleRaas) {  // refresh + evict -> the retained set of the next step
+        e = launch_raas_update(raas_params(h, layer, batch), st, h->pdl);
+        if (e != cudaSuccess) return cuda_fail(h, e, "raas update launch");
+        ++h->launches;
+    }
     if (h->world > 1 && h->comm) {  // sequence sharding: all-gather the partials, then merge
         delta_status s2 = shard_allgather(h, h->L.shard_send, h->L.shard_recv, h->L.shard_block, st);
         if (s2 != DELTA_OK) return s2;
@@ -669,6 +700,7 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
     for (int i = 0; i < cfg->num_select_layers; ++i) h->slot[cfg->select_layers[i]] = i;
     for (int l = 0; l < cfg->num_layers; ++l)
         if (h->role[l] == kRoleQuest) h->slot[l] = 0;  // each Quest layer's own plan, consumed at once
+        else if (h->role[l] == kRoleRaas) h->slot[l] = l;  // each RaaS layer's persistent retained set
     h->sms = num_sms_current();
     h->gs = cfg->num_q_heads / cfg->num_kv_heads;
     h->L = layout(h->cfg, h->sms);
@@ -1102,6 +1134,24 @@ delta_status delta_prefill(delta_t h, int32_t layer, int32_t batch, int32_t ntok
     return DELTA_OK;
 }
 
+delta_status delta_raas_reset(delta_t h, int32_t layer, int32_t batch, cudaStream_t stream) {
+    if (!h) return fail(nullptr, DELTA_ERR_USAGE, "null handle");
+    if (h->cfg.policy != DELTA_POLICY_RAAS) return fail(h, DELTA_ERR_USAGE, "not a RAAS handle");
+    if (batch < 1 || batch > h->cfg.max_batch) return fail(h, DELTA_ERR_USAGE, "batch out of range");
+    if (layer < -1 || layer >= h->cfg.num_layers) return fail(h, DELTA_ERR_USAGE, "layer out of range");
+    { delta_status j = join_host(h, stream); if (j != DELTA_OK) return j; }
+    const int l0 = layer < 0 ? 0 : layer, l1 = layer < 0 ? h->cfg.num_layers : layer + 1;
+    for (int l = l0; l < l1; ++l) {
+        if (h->role[l] != kRoleRaas) continue;
+        cudaError_t e = launch_raas_reset(raas_params(h, l, batch), stream, h->pdl);
+        if (e != cudaSuccess) return cuda_fail(h, e, "raas reset launch");
+        ++h->launches;
+        h->last_kind = delta_ctx::kLastAppend;
+        h->last_layer = l;
+    }
+    return DELTA_OK;
+}
+
 delta_status delta_workspace_region(delta_t h, int32_t which, void** ptr, size_t* bytes) {
     if (!h || !ptr || !bytes) return fail(h, DELTA_ERR_USAGE, "null argument");
     if (which == 0) {
@@ -1110,6 +1160,9 @@ delta_status delta_workspace_region(delta_t h, int32_t which, void** ptr, size_t
     } else if (which == 1) {
         *ptr = h->ws + h->L.reps;
         *bytes = h->L.reps_bytes;
+    } else if (which == 2) {
+        *ptr = h->ws + h->L.raas_last;
+        *bytes = h->cfg.policy == DELTA_POLICY_RAAS ? (size_t)h->cfg.num_layers * h->cfg.max_batch * h->L.max_pages * 4 : 0;
     } else {
         return fail(h, DELTA_ERR_USAGE, "unknown workspace region");
     }

@@ -7,7 +7,7 @@
 
 namespace delta {
 
-enum Role : int { kRoleFull = 0, kRoleSelect = 1, kRoleSparse = 2, kRoleQuest = 3 };  // Quest: host role only
+enum Role : int { kRoleFull = 0, kRoleSelect = 1, kRoleSparse = 2, kRoleQuest = 3, kRoleRaas = 4 };  // 3, 4: host only
 enum DevErr : int { kDevOk = 0, kDevUsage = 2, kDevNumeric = 3, kDevCapacity = 4 };
 
 constexpr int kPage = 16;        // P
@@ -39,6 +39,7 @@ struct AttnParams {
     int prewait;        // 1: start geometry + KV stream before griddepcontrol.wait (see attn_tc.cu)
     int early_trigger;  // 1: launch_dependents right after the wait (else after the main loop)
     int cluster_policy; // cudaClusterSchedulingPolicy for the split-K cluster (0 = default)
+    int emit_logits;    // 1: write the scaled logits of the attended tokens and the LSE (SELECT, RaaS)
     int gmerge;         // 1: no cluster; one CTA per SM; splits merged through global memory by
                         //    the last-arriving CTA of each (sequence, kv head) (combine.cuh)
     float* gpart;       // gmerge: [batch][g][nsplit][gpart_floats(d)] split partials
@@ -173,6 +174,26 @@ struct PrefillParams {
 };
 cudaError_t launch_prefill(const PrefillParams& p, cudaStream_t st, bool pdl);
 size_t prefill_smem_bytes(int d, int gs);
+
+// RaaS policy (raas.cu): retained-set reset and the per-step refresh / eviction.
+struct RaasParams {
+    int m, g, layer, batch, max_batch, max_seq, max_pages, plan_cap, n_sink, n_window, k_pages;
+    int32_t* seq_len;           // raw counters n * g
+    const float* logits;        // [max_batch][max_seq][m] of the layer's attention this step
+    const float* lse;           // [max_batch][m]
+    int32_t* plan_idx;          // [max_batch][plan_cap] retained pages, ascending (this layer's slot)
+    int32_t* plan_phys;
+    int32_t* plan_count;
+    int32_t* plan_stamp;
+    int32_t* last;              // [max_batch][max_pages] last-salient step (this layer)
+    float* scores;              // [max_batch][max_units] page scores (exported)
+    int max_units;
+    const int32_t* block_table;
+    int bt_stride;
+    int32_t* ticket;            // [L][max_batch] arrival tickets (shared with the multi-CTA append)
+};
+cudaError_t launch_raas_reset(const RaasParams& p, cudaStream_t st, bool pdl);
+cudaError_t launch_raas_update(const RaasParams& p, cudaStream_t st, bool pdl);
 
 // Launchers (attn_tc.cu / attn_simt.cu / select.cu / append.cu).  Each returns the
 // cudaError_t of the launch.  `pdl` enables programmatic dependent launch.
