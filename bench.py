@@ -72,23 +72,36 @@ class ClockSampler:
         self.t = None
         self.err = None
 
-    def _run(self):
+    def _run(self, hd):
         import pynvml
         try:
-            pynvml.nvmlInit()
-            hd = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(hd, pynvml.NVML_CLOCK_SM))
             while True:
                 self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(hd, pynvml.NVML_CLOCK_SM)))
                 self.bits |= int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(hd))
+                self._first.set()
                 if self._stop.wait(0.002):
                     break
         except Exception as e:  # noqa: BLE001
             self.err = repr(e)
+            self._first.set()
 
     def start(self):
-        self.t = threading.Thread(target=self._run, daemon=True)
+        """NVML is initialised here, before the timed region; returns once the sampler has taken
+        its first sample, so the samples cover the region that follows."""
+        self._first = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            hd = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(hd, pynvml.NVML_CLOCK_SM))
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+            return
+        self.t = threading.Thread(target=self._run, args=(hd,), daemon=True)
         self.t.start()
+        self._first.wait(timeout=2.0)
+        self.sm.clear()  # keep only samples taken from here on
+        self.bits = 0
 
     def stop(self):
         self._stop.set()
