@@ -76,6 +76,32 @@ def test_config_errors(bad):
         d200.query_sizes(_c1(**bad))
 
 
+@pytest.mark.parametrize("policy", [d200.POLICY_QUEST, d200.POLICY_RAAS], ids=["quest", "raas"])
+@pytest.mark.parametrize("bad", [
+    dict(),                                     # Delta layers are not part of these policies
+    dict(select_layers=[], select_block=1),     # they work on pages
+    dict(select_layers=[], kv_dtype=d200.DELTA_FP32),
+    dict(select_layers=[], shard_world=2, shard_rank=0),
+], ids=["delta-layers", "token-mode", "fp32", "sharded"])
+def test_policy_config_errors(policy, bad):
+    """Quest / RaaS restrictions are CONFIG errors (include/delta.h)."""
+    with pytest.raises(DeltaError, match="CONFIG"):
+        d200.query_sizes(_c1(policy=policy, **bad))
+
+
+def test_policy_workspace_sizes():
+    """Quest adds the page representatives (L x pages x g x 2 x d bf16); RaaS the per-layer
+    plans (one per layer, every page) and last-salient steps."""
+    _, ws_delta = d200.query_sizes(_c1())
+    _, ws_quest = d200.query_sizes(_c1(policy=d200.POLICY_QUEST, select_layers=[]))
+    _, ws_raas = d200.query_sizes(_c1(policy=d200.POLICY_RAAS, select_layers=[]))
+    reps = 32 * 2052 * 8 * 2 * 128 * 2
+    assert ws_quest - ws_delta >= reps - (1 << 20)
+    assert ws_raas > ws_delta
+    with pytest.raises(DeltaError, match="CONFIG"):
+        d200.query_sizes(_c1(policy=7))
+
+
 def test_null_handle_calls_are_usage_errors():
     lib = d200.load_library()
     assert lib.delta_decode_layer(None, 0, 1, None, None, None, None) == 2

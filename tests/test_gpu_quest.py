@@ -199,3 +199,25 @@ def test_quest_config_errors():
     cfg.select_block = 1
     with pytest.raises(DeltaError):
         query_sizes(cfg)
+
+
+def test_quest_reps_after_prefill_chunk():
+    """A chunk appended by delta_prefill (multi-CTA append: 4 pages per CTA) folds every token
+    into its page's min/max: reps bit-exact with the oracle, and the next Quest decode step
+    matches the oracle."""
+    shape, seed, n0, ntok = QUEST_SMALL, 53, 1000, 300
+    case = QuestCase(shape, seed, batch=2, s_pre=n0, max_seq=n0 + ntok + 64)
+    for l in range(shape.L):
+        q = np.stack([np.stack([synth.q_rows(seed, l, b, n0 + i + 1, shape.m, shape.d, "bf16")
+                                for i in range(ntok)]) for b in range(2)])
+        kn = np.stack([synth.kv_rows(seed, l, b, n0, n0 + ntok, shape.g, shape.d, "bf16", "k") for b in range(2)])
+        vn = np.stack([synth.kv_rows(seed, l, b, n0, n0 + ntok, shape.g, shape.d, "bf16", "v") for b in range(2)])
+        to = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).cuda()  # noqa: E731
+        out = torch.empty((2, ntok, shape.m, shape.d), dtype=torch.float32, device="cuda")
+        case.stack.prefill(l, to(q), to(kn), to(vn), out)
+    torch.cuda.synchronize()
+    _check_reps(case, n0 + ntok)
+    s = n0 + ntok + 1
+    out, lse, plans, keys = case.step(s)
+    _check_reps(case, s)
+    _check_layer(case, s, out, lse, plans, keys)
