@@ -328,3 +328,75 @@ def test_umma_fewhot_epochs(monkeypatch):
     case = GpuCase(sh, 8, batch=1, s_pre=4095, max_seq=4096, planting=plant)
     out, lse, plans = case.step_layers(4096)
     _check_step(case, 4096, out, lse, plans)
+
+
+# ---------------------------------------------------------------- edge cases
+
+def test_first_token_attends_itself():
+    """Degenerate case of Eq.4: the first token of an empty cache (fused append, s = 1) has a
+    single key, so softmax = 1 and every head's output is exactly its group's new V row; a
+    decode on an empty cache without an append is a sticky USAGE error."""
+    shape = Shape(L=2, m=32, g=8, d=128, F=2, delta=[], k=512, S=4, Lw=32, block=16, dtype="bf16")
+    case = GpuCase(shape, 91, batch=2, s_pre=0, max_seq=64)
+    q, k, v = case.inputs(1)
+    out = torch.empty((shape.L, 2, shape.m, shape.d), dtype=torch.float32, device="cuda")
+    for l in range(shape.L):
+        case.stack.append_decode_layer(l, k[l], v[l], q[l], out[l])
+    torch.cuda.synchronize()
+    assert case.stack.get_error() == 0
+    vf = v.float().cpu().numpy()                           # [L][B][g][d]
+    gs = shape.m // shape.g
+    for l in range(shape.L):
+        for b in range(2):
+            expect = np.repeat(vf[l, b], gs, axis=0)          # head j reads group j // gs
+            np.testing.assert_array_equal(out[l, b].cpu().numpy(), expect)
+    empty = GpuCase(shape, 92, batch=1, s_pre=0, max_seq=64)
+    q1, _, _ = empty.inputs(1)
+    o1 = torch.empty((1, shape.m, shape.d), dtype=torch.float32, device="cuda")
+    empty.stack.decode_layer(0, q1[0], o1)
+    assert empty.stack.get_error() == 2                       # DELTA_ERR_USAGE
+
+
+def test_ragged_batch_lengths():
+    """R22: sequences of one call at different lengths (one below the budget, so its plan is
+    every page (R12), one across a page boundary, one long), each against the oracle."""
+    from synth import device as sd
+    from helpers import BF16_MAX_ABS  # noqa: F401
+    shape = BF16_SMALL
+    seed, lens = 93, [300, 2048, 3001]                     # s after this step's append
+    case = GpuCase(shape, seed, batch=3, s_pre=max(lens), max_seq=3100)
+    case.stack.set_seq_lens([s - 1 for s in lens])
+    q = torch.empty((shape.L, 3, shape.m, shape.d), dtype=torch.bfloat16, device="cuda")
+    k = torch.empty((shape.L, 3, shape.g, shape.d), dtype=torch.bfloat16, device="cuda")
+    v = torch.empty_like(k)
+    sd.fill_queries(q, seed, range(shape.L), lens)
+    sd.fill_new_kv(k, v, seed, range(shape.L), [s - 1 for s in lens])
+    out = torch.empty((shape.L, 3, shape.m, shape.d), dtype=torch.float32, device="cuda")
+    cap = case.stack.plan_capacity
+    idx = torch.empty((3, cap), dtype=torch.int32, device="cuda")
+    cnt = torch.empty((3,), dtype=torch.int32, device="cuda")
+    for l in range(shape.L):
+        case.stack.append_decode_layer(l, k[l], v[l], q[l], out[l])
+        if l == 1:
+            case.stack.select(1, 3, idx_out=idx, count_out=cnt)
+    torch.cuda.synchronize()
+    assert case.stack.get_error() == 0
+    o = out.cpu().numpy()
+    for b, s in enumerate(lens):
+        ref = oracle_step(shape, seed, b, s)
+        plan = idx[b, : int(cnt[b])].cpu().numpy()
+        same = check_plan(plan, ref[1][2], ref[1][3], s, shape, False)
+        if s <= shape.k + shape.S + shape.Lw:
+            assert plan.tolist() == list(range(-(-s // 16)))   # budget covers the context
+        for l in range(shape.L):
+            if l >= 2 and not same:
+                continue
+            assert_close_bf16(o[l, b], ref[l][0], f"layer {l} seq {b} (s={s})")
+
+
+def test_gs16_two_head_tiles():
+    """The largest GQA group (gs = 16: two 8-head MMA tiles per KV group) against the oracle."""
+    shape = Shape(L=3, m=32, g=2, d=128, F=1, delta=[1], k=256, S=4, Lw=32, block=16, dtype="bf16")
+    case = GpuCase(shape, 95, batch=2, s_pre=1500, max_seq=1600)
+    out, lse, plans = case.step_layers(1501)
+    _check_step(case, 1501, out, lse, plans)
