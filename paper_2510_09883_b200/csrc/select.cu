@@ -19,7 +19,10 @@
 namespace delta {
 namespace {
 
-constexpr int kSelThreads = 512;
+#ifndef DELTA_SEL_THREADS
+#define DELTA_SEL_THREADS 512
+#endif
+constexpr int kSelThreads = DELTA_SEL_THREADS;  // 1024 measured: C1 select 10.8 vs 9.0 us, C3 equal
 constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kSmemUnits = 16384;  // keys cached in shared memory up to this many units
 
@@ -283,7 +286,7 @@ __device__ __forceinline__ int topk_regs(const SelectParams& p, int n_units, int
     return tot;
 }
 
-__global__ void __launch_bounds__(kSelThreads, 2) select_kernel(const SelectParams p) {
+__global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel(const SelectParams p) {
     extern __shared__ uint32_t sm_keys[];  // [kSmemUnits] (only when it fits)
     __shared__ int scratch[2 * kSelWarps + 1];
     __shared__ __align__(16) int hist2[4 * 256];  // radix histograms (4 buffers, see topk_regs)
@@ -419,9 +422,7 @@ __global__ void __launch_bounds__(kSelThreads, 2) select_kernel(const SelectPara
     const int n_cand = n_units - n_forced;
     int count = 0;
     constexpr int IPT = 8;  // old path: consecutive units per thread, one chunk = 4096 units
-    static_assert(kSelThreads == 512, "two histogram slots per thread");
-    hist2[tid] = 0;
-    hist2[tid + kSelThreads] = 0;
+    for (int i = tid; i < 4 * 256; i += kSelThreads) hist2[i] = 0;
     if (tid == 0) {
         s_and = 0xffffffffu;
         s_or = 0u;
