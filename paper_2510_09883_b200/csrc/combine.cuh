@@ -171,6 +171,55 @@ __device__ __forceinline__ void cluster_epilogue(const AttnParams& p, const floa
     uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage) + ClusterStage<D>::kBarOff);
     const uint32_t sO_u = smem_u32(sO), sM_u = smem_u32(sM), bar_u = smem_u32(bar);
     cluster_wait();  // pairs with the entry arrive: every peer's barrier is initialised
+    if (ns == 1) {
+        // a cluster of one CTA (one split): st.async needs a peer CTA, so fold the warp states
+        // and write the outputs directly
+        bool bad1 = false;
+        for (int idx = tid; idx < total; idx += nthreads) {
+            const int row = idx / C4, c4 = idx - row * C4;
+            float M = -INFINITY;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) M = fmaxf(M, ms[w * 16 + row]);
+            float L = 0.f;
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const float mw = ms[w * 16 + row];
+                const float f = (M == -INFINITY || mw == -INFINITY) ? 0.f : exp2f(mw - M);
+                const float4 v = reinterpret_cast<const float4*>(os + (w * OSROWS + row) * OS)[c4];
+                o.x += f * v.x; o.y += f * v.y; o.z += f * v.z; o.w += f * v.w;
+                L += ls[w * 16 + row] * f;
+            }
+            const float inv = (L > 0.f) ? __frcp_rn(L) : 0.f;
+            o = make_float4(o.x * inv, o.y * inv, o.z * inv, o.w * inv);
+            if (stale) {
+                const float qn = __int_as_float(0x7fc00000);  // NaN: stale plan must be loud
+                o = make_float4(qn, qn, qn, qn);
+            } else if (!(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w))) {
+                bad1 = true;
+            }
+            const int j = h * gs + row;
+            const bool shard = p.shard_world > 1;
+            reinterpret_cast<float4*>((shard ? p.part_o : p.out) + ((size_t)b * p.m + j) * D)[c4] = o;
+            if (c4 == 0) {
+                const float lse = (L > 0.f) ? (M + log2f(L)) * kLn2 : -INFINITY;
+                if (shard) {
+                    p.part_lse[(size_t)b * p.m + j] = lse;
+                } else {
+                    if (p.lse_out) p.lse_out[(size_t)b * p.m + j] = lse;
+                    if (p.emit_logits) p.lse_buf[(size_t)b * p.m + j] = lse;
+                }
+            }
+        }
+        if (bad1) set_err(p.err, kDevNumeric);
+        if (tid == 0) {
+            if (stale) set_err(p.err, kDevUsage);
+            if (cap_err) set_err(p.err, kDevCapacity);
+            if (s_post <= 0) set_err(p.err, kDevUsage);  // attention over an empty cache
+            if (p.fuse_append && !cap_err) atomicAdd(&p.seq_len[p.layer * p.max_batch + b], 1);
+        }
+        return;
+    }
     // 1. push
     for (int idx = tid; idx < total; idx += nthreads) {
         const int row = idx / C4, c4 = idx - row * C4;
