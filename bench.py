@@ -226,9 +226,25 @@ def cpu_baseline(c, cores=None):
         t += time.perf_counter() - t0
         reps += 1
     byts = reps * s * c["g"] * c["d"] * 4
+    # the same layer on one thread (the core count and a 1-thread number)
+    t1, reps1 = 0.0, 0
+    while t1 < 2.0:
+        t0 = time.perf_counter()
+        oracle.decode_heads(q, kv, s, scale, nthreads=1)
+        t1 += time.perf_counter() - t0
+        reps1 += 1
+    cpu_model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu_model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
     return {"value": round(byts / t / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
             "sample": f"{reps} x one FULL layer (all {c['m']} heads) of one sequence at s={s}, fp64, "
-                      f"{t:.1f} s of CPU time; KV generation untimed"}
+                      f"{t:.1f} s of CPU time; KV generation untimed",
+            "value_1thread": round(reps1 * s * c["g"] * c["d"] * 4 / t1 / 1e9, 4), "cpu": cpu_model}
 
 
 # ------------------------------------------------------------------ our arm
