@@ -154,6 +154,10 @@ delta_status delta_append_kv(delta_t h, int32_t layer, int32_t batch, int32_t nt
  *           softmax renormalised over rho (R10, R13).  USAGE error if
  *           that plan is stale (host check) — under graph replay the device check sets
  *           the sticky USAGE flag and writes NaN outputs.
+ *  QUEST  : page keys from the layer's min/max representatives and q, top-k pages, Eq.4 over
+ *           them (policy QUEST, see below).
+ *  RAAS   : Eq.4 over the layer's retained pages, then refresh / eviction for the next step
+ *           (policy RAAS, see below).
  * q: device [batch][m][d] kv_dtype.  out: device [batch][m][d] fp32.
  * lse_out: optional device [batch][m] fp32 natural-log LSE of each head's logits over
  * the attended set (NULL to skip). */
