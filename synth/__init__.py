@@ -98,6 +98,7 @@ class Planting:
     G: float          # Q boost (multiple of 0.5)
     lo: int           # first eligible unit
     hi: int           # one past the last eligible unit
+    shared: bool = False  # the same units in every layer (inter-layer correlation)
 
 
 def planted_units(seed: int, layer: int, seq: int, p: Planting) -> np.ndarray:
@@ -105,7 +106,8 @@ def planted_units(seed: int, layer: int, seq: int, p: Planting) -> np.ndarray:
         return np.zeros(0, np.int64)
     units = np.arange(p.lo, p.hi, dtype=np.int64)
     assert units.size >= p.count, "planting region too small"
-    h = splitmix64(np.uint64(stream_key(seed, TAG_PLANT, layer, seq)) + units.astype(np.uint64))
+    key_layer = 0 if p.shared else layer
+    h = splitmix64(np.uint64(stream_key(seed, TAG_PLANT, key_layer, seq)) + units.astype(np.uint64))
     order = np.lexsort((units, h))  # smallest hash, ties by index
     return np.sort(units[order[: p.count]])
 
