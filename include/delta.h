@@ -232,8 +232,9 @@ delta_status delta_copy_plan(delta_t h, int32_t layer, int32_t batch, int32_t* i
  * QUEST layer after its decode at this step: R_j = sum_{t in tokens(rho)} alpha_j(t) /
  * sum_{t < s} alpha_j(t), alpha_j = the layer's exact full-attention weights for its query q
  * ([batch][m][d] kv_dtype, the same q as the decode), rho = the plan the layer attended (its
- * own, the governing Delta layer's, or — QUEST — the plan of the latest decoded QUEST layer,
- * so call it right after that layer).  Runs a full-attention probe of the layer, which
+ * own, the governing Delta layer's, — QUEST — the plan of the latest decoded QUEST layer, so
+ * call it right after that layer, or — RAAS — the layer's retained set after this step's
+ * eviction).  Runs a full-attention probe of the layer, which
  * overwrites the Delta-layer logits / LSE buffers: call it after the step's delta_select
  * calls.  recall_out: device [batch][m] fp32.  Not sequence-sharded. */
 delta_status delta_attention_recall(delta_t h, int32_t layer, int32_t batch, const void* q, float* recall_out,
