@@ -339,6 +339,8 @@ def run_ours(args, c):
         if world > 1:
             dist.barrier()
 
+    stack_pct = {}
+
     def time_stack(stack, clocks=None):
         stack.set_seq_lens([s_pre] * batch)
         if stack is raas:
@@ -353,16 +355,23 @@ def run_ours(args, c):
         torch.cuda.synchronize()
         if clocks:
             clocks.start()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(K - 1)]  # per-step boundaries
         with torch.cuda.stream(stream):
             ev0.record(stream)
-            for i in range(W, W + K):
+            for j, i in enumerate(range(W, W + K)):
                 stack.decode_step(q_all[i], k_all[i], v_all[i], out, stream=stream)
+                if j < K - 1:
+                    evs[j].record(stream)
             ev1.record(stream)
         stream.synchronize()
         torch.cuda.synchronize()
         barrier()
         clk = clocks.stop() if clocks else None
         ms = ev0.elapsed_time(ev1)
+        marks = [ev0] + evs + [ev1]
+        steps_us = sorted(1e3 * marks[j].elapsed_time(marks[j + 1]) for j in range(K))
+        pct = {"p50": round(steps_us[len(steps_us) // 2], 2), "p90": round(steps_us[min(K - 1, (9 * K) // 10)], 2)}
+        stack_pct[id(stack)] = pct
         return ms, stack.kernels_launched - launched0, clk
 
     clocks = ClockSampler(local)
@@ -515,6 +524,8 @@ def run_ours(args, c):
                    "delta_layers": c["delta"], "full_prefix": c["F"], "parallelism": (f"sequence-shard x{world} (NCCL)" if seq_shard else f"batch-shard x{world}"),
                    "l2": "inputs larger than L2: >= 861 MB of KV read per step vs 126 MB L2 (no flush)"},
         "decode_step_us": round(1e3 * ms_delta / K, 2),
+        "decode_step_us_pct": stack_pct.get(id(delta)),
+        "full_stack_us_pct": stack_pct.get(id(full)),
         "full_stack_us": round(1e3 * ms_full / K, 2),
         "speedup_vs_full": round(ms_full / ms_delta, 3),
         "quest_stack_us": round(1e3 * ms_quest / K, 2) if ms_quest else None,
