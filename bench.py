@@ -233,6 +233,28 @@ def cpu_baseline(c, cores=None):
         oracle.decode_heads(q, kv, s, scale, nthreads=1)
         t1 += time.perf_counter() - t0
         reps1 += 1
+    # the other roles of a step, sampled on the same sequence, for an extrapolated oracle step
+    # time at this config (C2-C4 are too large to run whole on the host)
+    cfg_o = oracle.StackConfig(num_layers=c["L"], m=c["m"], g=c["g"], d=c["d"], page_size=PAGE,
+                               num_full_prefix=c["F"], select_layers=c["delta"], budget_k=c["k"], n_sink=S_SINK,
+                               n_window=L_WIN, select_block=PAGE, scale=scale)
+    t_delta, reps_d, toks = 0.0, 0, None
+    while t_delta < 3.0 or reps_d < 2:
+        t0 = time.perf_counter()
+        _, _, alpha = oracle.decode_heads(q, kv, s, scale, want_alpha=True, nthreads=cores)
+        _, units = oracle.select_from_alpha(cfg_o, alpha, s)
+        t_delta += time.perf_counter() - t0
+        reps_d += 1
+        toks = oracle.units_to_tokens(units, PAGE, s)
+    t_sp, reps_s = 0.0, 0
+    while t_sp < 1.0 or reps_s < 3:
+        t0 = time.perf_counter()
+        oracle.decode_heads(q, kv, toks, scale, nthreads=cores)
+        t_sp += time.perf_counter() - t0
+        reps_s += 1
+    t_f1, t_d1, t_s1 = t / reps, t_delta / reps_d, t_sp / reps_s
+    n_sp = c["L"] - c["F"] - len(c["delta"])
+    per_seq = c["F"] * t_f1 + len(c["delta"]) * t_d1 + n_sp * t_s1
     cpu_model = ""
     try:
         for line in open("/proc/cpuinfo"):
@@ -244,7 +266,13 @@ def cpu_baseline(c, cores=None):
     return {"value": round(byts / t / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
             "sample": f"{reps} x one FULL layer (all {c['m']} heads) of one sequence at s={s}, fp64, "
                       f"{t:.1f} s of CPU time; KV generation untimed",
-            "value_1thread": round(reps1 * s * c["g"] * c["d"] * 4 / t1 / 1e9, 4), "cpu": cpu_model}
+            "value_1thread": round(reps1 * s * c["g"] * c["d"] * 4 / t1 / 1e9, 4), "cpu": cpu_model,
+            "oracle_step_s_extrapolated": {
+                "delta": round(c["batch"] * per_seq, 3), "full": round(c["batch"] * c["L"] * t_f1, 3),
+                "per_sequence_layer_s": {"full": round(t_f1, 4), "delta_incl_score_topk": round(t_d1, 4),
+                                         "sparse": round(t_s1, 5)},
+                "how": (f"extrapolated: batch {c['batch']} x (F={c['F']} full + {len(c['delta'])} Delta (full + score + "
+                        f"top-k) + {n_sp} sparse layers), each timed on one sampled sequence/layer at s={s}")}}
 
 
 # ------------------------------------------------------------------ our arm
@@ -281,12 +309,12 @@ def run_ours(args, c):
     max_seq = s_first + K + PAGE
     seed = 2511 if seq_shard else 2511 + 1000 * rank  # batch sharding: every rank its own sequences
 
-    def make_cfg(full: bool, quest: bool = False, raas: bool = False):
+    def make_cfg(full: bool, quest: bool = False, raas: bool = False, budget: int | None = None):
         return d200.DeltaConfig(num_layers=c["L"], num_q_heads=c["m"], num_kv_heads=c["g"], head_dim=c["d"],
                                 max_batch=batch, max_seq_len=max_seq,
                                 num_full_prefix=c["L"] if full else c["F"],
                                 select_layers=[] if (full or quest or raas) else c["delta"],
-                                budget_k=c["k"], n_sink=S_SINK, n_window=L_WIN, select_block=PAGE,
+                                budget_k=budget or c["k"], n_sink=S_SINK, n_window=L_WIN, select_block=PAGE,
                                 shard_world=world if seq_shard else 1, shard_rank=rank if seq_shard else 0,
                                 nccl_id=nccl_ids[1 if full else 0],
                                 policy=(d200.POLICY_QUEST if quest else d200.POLICY_RAAS if raas else d200.POLICY_DELTA))
@@ -341,15 +369,22 @@ def run_ours(args, c):
 
     stack_pct = {}
 
+    # One set of device input buffers for every warm-up and timed step (q_all[W] etc. are fixed
+    # views), so delta_decode_step captures its graph once, during warm-up, and the timed loop is
+    # pure graph replays (asserted with the library's capture counter).  Each step still appends
+    # its row at the next position (s grows by one per step).
+    q_fix, k_fix, v_fix = q_all[W], k_all[W], v_all[W]
+
     def time_stack(stack, clocks=None):
         stack.set_seq_lens([s_pre] * batch)
         if stack is raas:
             stack.raas_reset(-1, batch, stream=stream)  # every page retained; warm-up steps evict to the budget
         with torch.cuda.stream(stream):
             for i in range(W):
-                stack.decode_step(q_all[i], k_all[i], v_all[i], out, stream=stream)
+                stack.decode_step(q_fix, k_fix, v_fix, out, stream=stream)
         stream.synchronize()
         launched0 = stack.kernels_launched
+        captures0 = stack.graph_captures
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         torch.cuda.synchronize()
@@ -358,8 +393,8 @@ def run_ours(args, c):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(K - 1)]  # per-step boundaries
         with torch.cuda.stream(stream):
             ev0.record(stream)
-            for j, i in enumerate(range(W, W + K)):
-                stack.decode_step(q_all[i], k_all[i], v_all[i], out, stream=stream)
+            for j in range(K):
+                stack.decode_step(q_fix, k_fix, v_fix, out, stream=stream)
                 if j < K - 1:
                     evs[j].record(stream)
             ev1.record(stream)
@@ -372,6 +407,7 @@ def run_ours(args, c):
         steps_us = sorted(1e3 * marks[j].elapsed_time(marks[j + 1]) for j in range(K))
         pct = {"p50": round(steps_us[len(steps_us) // 2], 2), "p90": round(steps_us[min(K - 1, (9 * K) // 10)], 2)}
         stack_pct[id(stack)] = pct
+        assert stack.graph_captures == captures0, "the timed region re-captured a graph (not pure replay)"
         return ms, stack.kernels_launched - launched0, clk
 
     clocks = ClockSampler(local)
@@ -385,6 +421,23 @@ def run_ours(args, c):
             assert e_other == 0, f"device error flag {e_other} (comparison stack)"
     err = delta.get_error()
     assert err == 0, f"device error flag {err}"
+
+    # ---- budget sweep (PAPER.md:217-223's budget axis): DELTA(k) vs the same Full
+    sweep = []
+    for kb in ([int(x) for x in args.budget.split(",")] if args.budget else []):
+        bcfg = make_cfg(False, budget=kb)
+        _, bws = d200.query_sizes(bcfg)
+        bst = d200.DeltaStack(bcfg, delta.kv_pool, delta.block_table, torch.zeros(bws, dtype=torch.uint8, device=dev))
+        ms_b = time_stack(bst)[0]
+        assert bst.get_error() == 0
+        bst.close()
+        bb = bf = 0
+        for i in range(K):
+            sb = step_bytes(c, s_first + i, batch, sparse_token_count(s_first + i, kb))
+            bb += sb["delta"]
+            bf += sb["full_stack"]
+        sweep.append({"budget_k": kb, "delta_us": round(1e3 * ms_b / K, 2), "speedup_vs_full": round(ms_full / ms_b, 3),
+                      "byte_ratio": round(bf / bb, 3), "speedup_target": round(0.8 * bf / bb, 3)})
 
     # max over ranks
     def max_over_ranks(x: float) -> float:
@@ -468,19 +521,89 @@ def run_ours(args, c):
     kbytes = batch * s_last * g * d * 2 * 2
     n_sp_tok = sparse_token_count(s_last, c["k"])
     sp_bytes = batch * (n_sp_tok * g * d * 2 * 2 + (n_sp_tok // PAGE) * 4)
-    us_kernel = us_full
     peak, peak_src = measured_peaks()
-    achieved = kbytes / (us_kernel * 1e-6) / 1e9
-    roof_bytes, roof_how = kbytes, "eager back-to-back launches of layer 0 (CUDA events on the stream)"
+
+    # ---- in-graph launch durations (the DELTA step is a graph of PDL-chained kernels; eager
+    # back-to-back launches are not the same thing).  FULL: the Full stack's timed region is
+    # nothing but FULL-layer launches -> region time / launches.  SPARSE: two graph-replayed
+    # stacks on the same pools that differ only in their number of sparse layers (layer 0 SELECT
+    # governing layers 1..L-1, with L = 32 and L = 4): (t_32 - t_4) / 28 sparse launches.
+    def chain_us(n_layers):
+        ccfg = d200.DeltaConfig(num_layers=n_layers, num_q_heads=m, num_kv_heads=g, head_dim=d, max_batch=batch,
+                                max_seq_len=max_seq, num_full_prefix=0, select_layers=[0], budget_k=c["k"],
+                                n_sink=S_SINK, n_window=L_WIN, select_block=PAGE)
+        _, cws = d200.query_sizes(ccfg)
+        st_ = d200.DeltaStack(ccfg, delta.kv_pool, delta.block_table,  # layers [0, n) of the same pools
+                              torch.zeros(cws, dtype=torch.uint8, device=dev))
+        st_.set_seq_lens([s_pre] * batch)
+        qn, kn, vn = q_fix[:n_layers], k_fix[:n_layers], v_fix[:n_layers]
+        with torch.cuda.stream(stream):
+            for _ in range(W):
+                st_.decode_step(qn, kn, vn, out[:n_layers], stream=stream)
+        stream.synchronize()
+        cap0 = st_.graph_captures
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(K):
+                st_.decode_step(qn, kn, vn, out[:n_layers], stream=stream)
+            e1.record(stream)
+        stream.synchronize()
+        assert st_.graph_captures == cap0 and st_.get_error() == 0
+        st_.close()
+        return 1e3 * e0.elapsed_time(e1) / K
+
+    us_full_graph = 1e3 * ms_full / (c["L"] * K) if not seq_shard else us_full
+    us_sparse_graph = None
     if not seq_shard:
-        # the Full stack's timed region is nothing but FULL-layer launches of this kernel (graph
-        # replay with PDL): its average launch duration there = region time / launches
-        n_launch = c["L"] * K
-        us_kernel = 1e3 * ms_full / n_launch
-        roof_bytes = byts_full / n_launch
-        achieved = roof_bytes / (us_kernel * 1e-6) / 1e9
-        roof_how = (f"the Full stack's timed region: {n_launch} FULL-layer launches (graph replay, PDL), "
-                    f"device time / launches; eager back-to-back launch {us_full:.3f} us")
+        us_sparse_graph = (chain_us(32) - chain_us(4)) / 28.0
+    us_step = 1e3 * ms_delta / K
+    n_fullcache = c["F"] + len(c["delta"])
+    n_sparse_l = c["L"] - n_fullcache
+    breakdown = {"full_cache_layers_us": round(n_fullcache * us_full_graph, 1)}
+    if us_sparse_graph is not None:
+        breakdown["sparse_layers_us"] = round(n_sparse_l * us_sparse_graph, 1)
+        breakdown["select_and_rest_us"] = round(us_step - n_fullcache * us_full_graph - n_sparse_l * us_sparse_graph, 1)
+        breakdown["select_per_delta_layer_us"] = round(breakdown["select_and_rest_us"] / len(c["delta"]), 2)
+    breakdown["how"] = ("in-graph per-launch durations x launches: FULL from the Full stack's region, SPARSE from "
+                        "(t(L=32) - t(L=4)) / 28 of two graph-replayed SELECT+SPARSE chains on the same pools; "
+                        "select_and_rest = the DELTA step minus both (the three score+top-k launches, and the "
+                        "first sparse layer after each of them, which cannot prefetch its plan's pages)")
+
+    # ---- pure-read roofline reference measured in this run (K10): stream the KV pool once
+    sink = torch.zeros(1, dtype=torch.float32, device=dev)
+    probe_bytes = delta.kv_pool.numel() * delta.kv_pool.element_size()
+    probe_us = []
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            d200.read_bandwidth_probe(delta.kv_pool, sink, stream=stream)
+            e1.record(stream)
+        stream.synchronize()
+        probe_us.append(1e3 * e0.elapsed_time(e1))
+    pure_read_gbs = probe_bytes / (min(probe_us[1:]) * 1e-6) / 1e9
+    NOMINAL_GBS = 8000.0  # north star "~8 TB/s"
+
+    def roof(kernel, nbytes, us, how, share):
+        a = nbytes / (us * 1e-6) / 1e9
+        return {"bound": "hbm", "achieved": round(a, 1), "peak": peak, "unit": "GB/s", "frac": round(a / peak, 4),
+                "frac_of_8tbs": round(a / NOMINAL_GBS, 4), "frac_of_pure_read": round(a / pure_read_gbs, 4),
+                "kernel": kernel, "algorithmic_bytes_per_launch": int(nbytes), "avg_launch_us": round(us, 3),
+                "share_of_step": round(share, 3) if share is not None else None, "measured": how,
+                "peak_source": peak_src}
+
+    roof_full = roof("attn_tc_kernel<128,false> FULL/SELECT (split-K, global merge), one layer", kbytes,
+                     us_full_graph, (f"in-graph: the Full stack's timed region, {c['L'] * K} FULL launches, device "
+                                     f"time / launches; eager back-to-back {us_full:.3f} us"),
+                     n_fullcache * us_full_graph / us_step)
+    if us_sparse_graph is not None:
+        roof_sparse = roof("sparse_lat_kernel<128> SPARSE (all tiles resident, cluster DSMEM merge), one layer",
+                           sp_bytes, us_sparse_graph,
+                           f"in-graph: (t(L=32) - t(L=4)) / 28 of two SELECT+SPARSE chains; eager {us_sparse:.3f} us",
+                           n_sparse_l * us_sparse_graph / us_step)
+    else:
+        roof_sparse = roof("SPARSE layer kernel, one layer (eager)", sp_bytes, us_sparse, "eager back-to-back", None)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_full_decode_traffic.json")
     if os.path.exists(prof):
@@ -488,6 +611,9 @@ def run_ours(args, c):
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    roof_full["traffic"] = traffic
+    # "roofline" = the kernel with the largest share of the DELTA step's time
+    dominant = roof_full if (roof_sparse["share_of_step"] or 0) <= roof_full["share_of_step"] else roof_sparse
     kernels = {
         "full_layer_us": round(us_full, 3), "full_layer_gbs": round(kbytes / (us_full * 1e-6) / 1e9, 1),
         "select_layer_decode_us": round(us_sel_dec, 3), "select_topk_us": round(us_select, 3),
@@ -534,19 +660,15 @@ def run_ours(args, c):
         "byte_ratio": round(byte_ratio, 3),
         "speedup_target": round(0.8 * byte_ratio, 3),
         "full_stack_gbs": round(byts_full * (1 if seq_shard else world) / (ms_full * 1e-3) / 1e9, 2),
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "attn_tc_kernel<128,false> FULL (global-merge split-K), one layer",
-                     "algorithmic_bytes_per_launch": int(roof_bytes), "avg_launch_us": round(us_kernel, 3),
-                     "measured": roof_how, "peak_source": peak_src},
-        # the SPARSE-layer kernel (27 of 32 layers at C1; the larger share of the DELTA step's time at b = 1)
-        "roofline_sparse": {"bound": "hbm", "achieved": round(sp_bytes / (us_sparse * 1e-6) / 1e9, 1), "peak": peak,
-                            "unit": "GB/s", "frac": round(sp_bytes / (us_sparse * 1e-6) / 1e9 / peak, 4),
-                            "kernel": "attn_tc_kernel<128,false> SPARSE (cluster split-K), one layer",
-                            "algorithmic_bytes_per_launch": sp_bytes, "avg_launch_us": round(us_sparse, 3)},
+        "roofline": dominant,
+        "roofline_full": roof_full,
+        "roofline_sparse": roof_sparse,
+        "pure_read_gbs": round(pure_read_gbs, 1),
+        "step_breakdown": breakdown,
         "kernels": kernels,
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": round(ms_e2e / K, 5)},
+        "budget_sweep": sweep or None,
         "gpu_launches": int(launches),
         "clocks": clk,
     }
@@ -565,6 +687,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--budget", default="", help="comma-separated token budgets for a DELTA(k) sweep, e.g. "
+                                                 "1024,2048,4096,8192 (reported as budget_sweep)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

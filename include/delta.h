@@ -296,6 +296,16 @@ delta_status delta_destroy(delta_t h);
  * enqueued since creation (graph replays count their kernels). */
 uint64_t     delta_kernels_launched(delta_t h);
 
+/* Number of CUDA-graph captures delta_decode_step has made (one per distinct input pointer
+ * set / stream / batch; replays add none) — lets a timing loop assert it measured pure replays. */
+uint64_t     delta_graph_captures(delta_t h);
+
+/* Measurement utility, not part of the method (SURVEY §8(d) "K10"): streams `bytes` of the
+ * device buffer `buf` once with 16-byte loads (a pure-read roofline reference measured in the
+ * same run as the decode kernels).  `sink` is a device float the kernel may write.  Enqueued on
+ * `stream`; returns USAGE for null pointers, CUDA on a launch failure. */
+delta_status delta_read_bandwidth_probe(const void* buf, size_t bytes, float* sink, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,10 +5,11 @@ The product is ``libdelta.so`` (C ABI in ``include/delta.h``; sm_100a kernels in
 """
 from .binding import (DELTA_BF16, DELTA_FP32, POLICY_DELTA, POLICY_QUEST, POLICY_RAAS, ROLE_FULL, ROLE_QUEST,
                       ROLE_RAAS, ROLE_SELECT, ROLE_SPARSE, DeltaConfig, DeltaError,
-                      DeltaStack, declared_functions, load_library, nccl_unique_id, query_sizes, shard_range)
+                      DeltaStack, declared_functions, load_library, nccl_unique_id, query_sizes, read_bandwidth_probe,
+                      shard_range)
 
 __all__ = ["DELTA_BF16", "DELTA_FP32", "POLICY_DELTA", "POLICY_QUEST", "POLICY_RAAS", "ROLE_FULL", "ROLE_QUEST",
            "ROLE_RAAS", "ROLE_SELECT",
            "ROLE_SPARSE", "DeltaConfig", "DeltaError",
            "DeltaStack", "declared_functions", "load_library", "nccl_unique_id", "query_sizes",
-           "shard_range"]
+           "read_bandwidth_probe", "shard_range"]

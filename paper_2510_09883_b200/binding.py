@@ -95,6 +95,10 @@ def load_library() -> ctypes.CDLL:
     L.delta_destroy.restype = st
     L.delta_kernels_launched.argtypes = [vp]
     L.delta_kernels_launched.restype = ctypes.c_uint64
+    L.delta_graph_captures.argtypes = [vp]
+    L.delta_graph_captures.restype = ctypes.c_uint64
+    L.delta_read_bandwidth_probe.argtypes = [vp, ctypes.c_size_t, vp, vp]
+    L.delta_read_bandwidth_probe.restype = st
     L.delta_nccl_get_unique_id.argtypes = [vp]
     L.delta_nccl_get_unique_id.restype = st
     L.delta_shard_range.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(i32), ctypes.POINTER(i32)]
@@ -206,6 +210,14 @@ def shard_range(cfg: DeltaConfig) -> tuple[int, int]:
     lo, hi = ctypes.c_int32(), ctypes.c_int32()
     _check(load_library().delta_shard_range(ctypes.byref(c), ctypes.byref(lo), ctypes.byref(hi)))
     return lo.value, hi.value
+
+
+def read_bandwidth_probe(buf, sink, stream=None):
+    """Pure-read roofline kernel (measurement utility): streams the device
+    tensor `buf` once; `sink` is a 1-element fp32 device tensor."""
+    assert buf.is_cuda and sink.is_cuda and sink.dtype.is_floating_point
+    _check(load_library().delta_read_bandwidth_probe(buf.data_ptr(), buf.numel() * buf.element_size(),
+                                                      sink.data_ptr(), _stream(stream)))
 
 
 def _ptr(t) -> int | None:
@@ -350,6 +362,10 @@ class DeltaStack:
     @property
     def kernels_launched(self) -> int:
         return int(self.lib.delta_kernels_launched(self.h))
+
+    @property
+    def graph_captures(self) -> int:
+        return int(self.lib.delta_graph_captures(self.h))
 
     def close(self):
         if getattr(self, "h", None):

@@ -70,7 +70,7 @@ struct TcCfg {
 };
 
 template <int D, bool TOKEN_PLAN, int NSTAGE, int NH, int NG, bool CL>
-__global__ void __launch_bounds__(cta_threads<NG>(), (NH == 1 && CL) ? 2 : 1)  // cluster: two CTAs per SM
+__global__ void __launch_bounds__(cta_threads<NG>(), (NH == 1 && (CL || NSTAGE == kShallow)) ? 2 : 1)  // two CTAs per SM
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     static_assert(NSTAGE % NG == 0, "ring slots must map to fixed consumer groups");
     constexpr int NCW = NT * NG;  // consumer warps; warp NCW is the producer
@@ -539,6 +539,7 @@ constexpr int kGStage = 6, kGGroups = 3;
 template <int D, bool TOKEN_PLAN>
 cudaError_t launch_stages(const AttnParams& p, const CUtensorMap* tm_kv, cudaStream_t st,
                           bool pdl) {
+    if (p.gmerge && p.gm_shallow && p.gs <= 8) return launch_impl<D, TOKEN_PLAN, kShallow, 1, 2, false>(p, tm_kv, st, pdl);
     if (p.gmerge)
         return p.gs <= 8 ? launch_impl<D, TOKEN_PLAN, kGStage, 1, kGGroups, false>(p, tm_kv, st, pdl)
                          : launch_impl<D, TOKEN_PLAN, kGStage, 2, kGGroups, false>(p, tm_kv, st, pdl);

@@ -313,6 +313,7 @@ struct delta_ctx {
     cudaStream_t hs_in = nullptr, hs_comp = nullptr, hs_out = nullptr;
     cudaEvent_t hev_in[2] = {}, hev_done[2] = {}, hev_out[2] = {}, hev_join = nullptr;
     uint64_t launches = 0;
+    uint64_t captures = 0;  // decode-step graph captures (a timed loop of replays must not add any)
     bool pdl = true;
     int tune_nsplit = 0, tune_deep = -1;  // DELTA_TUNE overrides (0 / -1 = automatic)
     int tune_snsplit = 0;                 // sparse layers only
@@ -320,7 +321,7 @@ struct delta_ctx {
     // cycles to issue (tools/umma_test.cu), so 10 per tile lose to the mma.sync kernel here;
     // kept selectable (DELTA_TUNE umma=1) and parity-tested.
     int tune_prewait = 1, tune_early = 1, tune_umma = 0, tune_policy = 0;
-    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1;
+    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1, tune_gm2 = 0, tune_lat = 1, tune_qpf = 1;
     // sequence sharding
     int world = 1, rank = 0, page_lo = 0, page_hi = 0x7fffffff;
     ncclComm_t comm = nullptr;  // null with world > 1: the caller exchanges (delta_shard_* calls)
@@ -403,10 +404,25 @@ AttnParams attn_params(delta_ctx* h, int layer, int batch, int role_override = -
         p.nsplit = nsplit_gmerge(batch, c.num_kv_heads, h->sms, items);
         p.gpart = h->at<float>(h->L.gpart);
         p.gcnt = h->at<unsigned long long>(h->L.gcnt);
+        p.gm_shallow = h->tune_gm2;
     }
     const int cap = p.gmerge ? std::min(kMaxSplitG, h->L.gslots / std::max(1, batch * c.num_kv_heads)) : kMaxSplit;
     if (h->tune_nsplit > 0) p.nsplit = std::min(h->tune_nsplit, cap);
     if (h->tune_snsplit > 0 && p.role == kRoleSparse) p.nsplit = std::min(h->tune_snsplit, cap);
+    // SPARSE page plans at small batch: the latency kernel (attn_sparse.cu) when every split's
+    // share of the plan fits its resident tiles and two layers' CTAs fit one wave
+    if (p.role == kRoleSparse && !p.emit_logits && h->use_tc && !h->tune_umma && h->tune_lat &&
+        c.select_block == kPage && h->world == 1 && h->gs <= 8) {
+        const int lim = sparse_lat_max_split(c.head_dim);
+        int ns = h->tune_snsplit > 0 ? h->tune_snsplit : 12;
+        ns = std::min(ns, lim);
+        const int tiles = plan_tiles(c, h->L.plan_cap);
+        if (ns >= 1 && (tiles + ns - 1) / ns <= sparse_lat_max_tiles() && batch * c.num_kv_heads * ns <= h->sms) {
+            p.sparse_lat = 1;
+            p.gmerge = 0;
+            p.nsplit = ns;
+        }
+    }
     p.deep = deep_ring(batch, c.num_kv_heads, p.nsplit, h->sms) ? 1 : 0;
     if (h->tune_deep >= 0) p.deep = h->tune_deep;
     return p;
@@ -540,6 +556,7 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
     // this order; eager calls may follow other work on the stream.
     p.prewait = (in_step && h->tune_prewait) ? 1 : 0;
     p.early_trigger = h->tune_early;
+    p.q_prefetch = h->tune_qpf;
     p.cluster_policy = h->tune_policy;
     if (h->last_kind == delta_ctx::kLastNone) p.prewait = 0;
     if (h->last_layer == layer && (h->last_kind == delta_ctx::kLastAppend || h->last_kind == delta_ctx::kLastAttn))
@@ -549,6 +566,7 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
     // bf16: the tcgen05/TMEM kernel for GQA groups of <= 8 heads, the mma.sync kernel otherwise;
     // fp32 caches: the CUDA-core kernel (no tensor-core rounding of fp32 inputs).
     cudaError_t e = !h->use_tc ? launch_attn_simt(p, h->cfg.kv_dtype == DELTA_BF16, st, h->pdl)
+                    : p.sparse_lat ? launch_attn_sparse_lat(p, &h->tm_kv, st, h->pdl)
                     : (h->tune_umma && umma_supported(p)) ? launch_attn_umma(p, &h->tm_kv, st, h->pdl)
                                                           : launch_attn_tc(p, &h->tm_kv, st, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "decode launch");
@@ -795,6 +813,9 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
         if (const char* w = std::strstr(t, "seltrig=")) h->tune_seltrig = std::atoi(w + 8);
         if (const char* w = std::strstr(t, "gmerge=")) h->tune_gmerge = std::atoi(w + 7);
         if (const char* w = std::strstr(t, "selhist=")) h->tune_selhist = std::atoi(w + 8);
+        if (const char* w = std::strstr(t, "gm2=")) h->tune_gm2 = std::atoi(w + 4);
+        if (const char* w = std::strstr(t, "lat=")) h->tune_lat = std::atoi(w + 4);
+        if (const char* w = std::strstr(t, "qpf=")) h->tune_qpf = std::atoi(w + 4);
     }
     h->step.assign(cfg->num_layers, 0);
     h->dec_step.assign(cfg->num_layers, -1);
@@ -943,6 +964,7 @@ delta_status delta_decode_step(delta_t h, int32_t batch, const void* q_all, cons
             if (s != DELTA_OK) { if (graph) cudaGraphDestroy(graph); return s; }
             if (e != cudaSuccess) return cuda_fail(h, e, "graph capture end");
             ge->kernels = h->launches - before;
+            ++h->captures;
             h->launches = before;
             e = cudaGraphInstantiate(&ge->exec, graph, 0);
             cudaGraphDestroy(graph);
@@ -1198,6 +1220,15 @@ int32_t delta_plan_capacity(delta_t h) { return h ? h->L.plan_cap : -1; }
 const char* delta_last_error_message(delta_t h) { return h ? h->msg.c_str() : g_msg.c_str(); }
 
 uint64_t delta_kernels_launched(delta_t h) { return h ? h->launches : 0; }
+
+uint64_t delta_graph_captures(delta_t h) { return h ? h->captures : 0; }
+
+delta_status delta_read_bandwidth_probe(const void* buf, size_t bytes, float* sink, cudaStream_t stream) {
+    if (!buf || !sink) return fail(nullptr, DELTA_ERR_USAGE, "null buffer");
+    cudaError_t e = launch_read_probe(buf, bytes, sink, num_sms_current(), stream);
+    if (e != cudaSuccess) return fail(nullptr, DELTA_ERR_CUDA, std::string("read probe: ") + cudaGetErrorString(e));
+    return DELTA_OK;
+}
 
 delta_status delta_nccl_get_unique_id(void* out_128_bytes) {
     if (!out_128_bytes) return fail(nullptr, DELTA_ERR_USAGE, "null argument");

@@ -5,7 +5,27 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace delta {
+
+// Per-device one-time kernel setup (cudaFuncSetAttribute opt-ins are per device context): the
+// cached value (> 0) of init() for the current device; init() returning <= 0 is not cached.
+constexpr int kMaxDevices = 64;
+template <typename F>
+int per_device_once(std::atomic<int>* cache, F init) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+        cudaGetLastError();
+        dev = 0;
+    }
+    int v = cache[dev].load(std::memory_order_acquire);
+    if (v <= 0) {
+        v = init();  // idempotent: a racing first call repeats it and stores the same value
+        if (v > 0) cache[dev].store(v, std::memory_order_release);
+    }
+    return v;
+}
 
 enum Role : int { kRoleFull = 0, kRoleSelect = 1, kRoleSparse = 2, kRoleQuest = 3, kRoleRaas = 4 };  // 3, 4: host only
 enum DevErr : int { kDevOk = 0, kDevUsage = 2, kDevNumeric = 3, kDevCapacity = 4 };
@@ -42,6 +62,10 @@ struct AttnParams {
     int emit_logits;    // 1: write the scaled logits of the attended tokens and the LSE (SELECT, RaaS)
     int gmerge;         // 1: no cluster; one CTA per SM; splits merged through global memory by
                         //    the last-arriving CTA of each (sequence, kv head) (combine.cuh)
+    int q_prefetch;     // 1: prefetch this CTA's q rows into L2 before griddepcontrol.wait
+    int sparse_lat;     // host: SPARSE layer takes the latency kernel (attn_sparse.cu)
+    int gm_shallow;     // gmerge: 1 = shallow ring (two CTAs per SM: the next layer's CTAs co-reside
+                        //    and prefetch during this one), 0 = deep ring (one CTA per SM)
     float* gpart;       // gmerge: [batch][g][nsplit][gpart_floats(d)] split partials
     unsigned long long* gcnt;  // gmerge: [max_batch][g][kMaxSplitG] ticket counters, by split count
     float scale;        // softmax scale (natural units)
@@ -198,6 +222,10 @@ cudaError_t launch_raas_update(const RaasParams& p, cudaStream_t st, bool pdl);
 // Launchers (attn_tc.cu / attn_simt.cu / select.cu / append.cu).  Each returns the
 // cudaError_t of the launch.  `pdl` enables programmatic dependent launch.
 cudaError_t launch_attn_tc(const AttnParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl);
+cudaError_t launch_read_probe(const void* buf, size_t bytes, float* sink, int sms, cudaStream_t st);
+cudaError_t launch_attn_sparse_lat(const AttnParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl);
+int sparse_lat_max_tiles();        // resident tiles per CTA of the latency kernel
+int sparse_lat_max_split(int d);   // largest co-resident cluster (split count) of the latency kernel
 cudaError_t launch_attn_umma(const AttnParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl);
 bool umma_supported(const AttnParams& p);
 cudaError_t launch_attn_simt(const AttnParams& p, bool bf16, cudaStream_t st, bool pdl);
