@@ -527,7 +527,7 @@ def run_ours(args, c):
     # back-to-back launches are not the same thing).  FULL: the Full stack's timed region is
     # nothing but FULL-layer launches -> region time / launches.  SPARSE: two graph-replayed
     # stacks on the same pools that differ only in their number of sparse layers (layer 0 SELECT
-    # governing layers 1..L-1, with L = 32 and L = 4): (t_32 - t_4) / 28 sparse launches.
+    # governing layers 1..n-1, with n = L and n = 4): (t_L - t_4) / (L - 4) sparse launches.
     def chain_us(n_layers):
         ccfg = d200.DeltaConfig(num_layers=n_layers, num_q_heads=m, num_kv_heads=g, head_dim=d, max_batch=batch,
                                 max_seq_len=max_seq, num_full_prefix=0, select_layers=[0], budget_k=c["k"],
@@ -556,7 +556,7 @@ def run_ours(args, c):
     us_full_graph = 1e3 * ms_full / (c["L"] * K) if not seq_shard else us_full
     us_sparse_graph = None
     if not seq_shard:
-        us_sparse_graph = (chain_us(32) - chain_us(4)) / 28.0
+        us_sparse_graph = (chain_us(c["L"]) - chain_us(4)) / (c["L"] - 4.0)
     us_step = 1e3 * ms_delta / K
     n_fullcache = c["F"] + len(c["delta"])
     n_sparse_l = c["L"] - n_fullcache
@@ -566,7 +566,7 @@ def run_ours(args, c):
         breakdown["select_and_rest_us"] = round(us_step - n_fullcache * us_full_graph - n_sparse_l * us_sparse_graph, 1)
         breakdown["select_per_delta_layer_us"] = round(breakdown["select_and_rest_us"] / len(c["delta"]), 2)
     breakdown["how"] = ("in-graph per-launch durations x launches: FULL from the Full stack's region, SPARSE from "
-                        "(t(L=32) - t(L=4)) / 28 of two graph-replayed SELECT+SPARSE chains on the same pools; "
+                        "(t(n=L) - t(n=4)) / (L - 4) of two graph-replayed SELECT+SPARSE chains on the same pools; "
                         "select_and_rest = the DELTA step minus both (the three score+top-k launches, and the "
                         "first sparse layer after each of them, which cannot prefetch its plan's pages)")
 
@@ -593,14 +593,13 @@ def run_ours(args, c):
                 "share_of_step": round(share, 3) if share is not None else None, "measured": how,
                 "peak_source": peak_src}
 
-    roof_full = roof("attn_tc_kernel<128,false> FULL/SELECT (split-K, global merge), one layer", kbytes,
+    roof_full = roof(f"FULL/SELECT layer: {delta.kernel_name(0, batch)}", kbytes,
                      us_full_graph, (f"in-graph: the Full stack's timed region, {c['L'] * K} FULL launches, device "
                                      f"time / launches; eager back-to-back {us_full:.3f} us"),
                      n_fullcache * us_full_graph / us_step)
     if us_sparse_graph is not None:
-        roof_sparse = roof("sparse_lat_kernel<128> SPARSE (all tiles resident, cluster DSMEM merge), one layer",
-                           sp_bytes, us_sparse_graph,
-                           f"in-graph: (t(L=32) - t(L=4)) / 28 of two SELECT+SPARSE chains; eager {us_sparse:.3f} us",
+        roof_sparse = roof(f"SPARSE layer: {delta.kernel_name(sp, batch)}", sp_bytes, us_sparse_graph,
+                           f"in-graph: (t(n={c['L']}) - t(n=4)) / {c['L'] - 4} of two SELECT+SPARSE chains; eager {us_sparse:.3f} us",
                            n_sparse_l * us_sparse_graph / us_step)
     else:
         roof_sparse = roof("SPARSE layer kernel, one layer (eager)", sp_bytes, us_sparse, "eager back-to-back", None)

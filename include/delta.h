@@ -300,6 +300,16 @@ uint64_t     delta_kernels_launched(delta_t h);
  * set / stream / batch; replays add none) — lets a timing loop assert it measured pure replays. */
 uint64_t     delta_graph_captures(delta_t h);
 
+/* Which attention kernel variant a decode of `layer` at `batch` launches (for reports); "" for
+ * a bad handle / layer / batch.  The string is static. */
+const char*  delta_layer_kernel_name(delta_t h, int32_t layer, int32_t batch);
+
+/* Experiment hook (tools/, never needed for correct results): override one kernel-variant knob
+ * of a handle (nsplit, snsplit, deep, prewait, early, umma, policy, seltrig, selhist, gmerge,
+ * gm2, lat, qpf — see DESIGN.md §7).  Drops the handle's captured step graphs.  CONFIG
+ * for an unknown key, USAGE for a null handle.  The library reads no environment variables. */
+delta_status delta_set_tuning(delta_t h, const char* key, int32_t value);
+
 /* Measurement utility, not part of the method (SURVEY §8(d) "K10"): streams `bytes` of the
  * device buffer `buf` once with 16-byte loads (a pure-read roofline reference measured in the
  * same run as the decode kernels).  `sink` is a device float the kernel may write.  Enqueued on

@@ -95,6 +95,10 @@ def load_library() -> ctypes.CDLL:
     L.delta_destroy.restype = st
     L.delta_kernels_launched.argtypes = [vp]
     L.delta_kernels_launched.restype = ctypes.c_uint64
+    L.delta_set_tuning.argtypes = [vp, ctypes.c_char_p, i32]
+    L.delta_set_tuning.restype = st
+    L.delta_layer_kernel_name.argtypes = [vp, i32, i32]
+    L.delta_layer_kernel_name.restype = ctypes.c_char_p
     L.delta_graph_captures.argtypes = [vp]
     L.delta_graph_captures.restype = ctypes.c_uint64
     L.delta_read_bandwidth_probe.argtypes = [vp, ctypes.c_size_t, vp, vp]
@@ -244,6 +248,15 @@ class DeltaStack:
         h = ctypes.c_void_p()
         _check(self.lib.delta_create(ctypes.byref(c), ctypes.byref(b), ctypes.byref(h)))
         self.h = h
+        import os
+        tune = os.environ.get("DELTA_TUNE", "")  # experiment knobs (tools/), "key=value,..."
+        for kv in filter(None, tune.split(",")):
+            k, v = kv.split("=")
+            self.set_tuning(k.strip(), int(v))
+
+    def set_tuning(self, key: str, value: int):
+        """Kernel-variant knob for experiments (delta_set_tuning)."""
+        _check(self.lib.delta_set_tuning(self.h, key.encode(), value), self.h)
 
     @property
     def k_pool(self):
@@ -362,6 +375,10 @@ class DeltaStack:
     @property
     def kernels_launched(self) -> int:
         return int(self.lib.delta_kernels_launched(self.h))
+
+    def kernel_name(self, layer: int, batch: int) -> str:
+        """The attention kernel variant a decode of `layer` at `batch` launches."""
+        return self.lib.delta_layer_kernel_name(self.h, layer, batch).decode()
 
     @property
     def graph_captures(self) -> int:

@@ -798,25 +798,6 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
             return fail(nullptr, DELTA_ERR_NCCL, m);
         }
     }
-    // Tuning hook for kernel experiments (tools/trace_probe.py): DELTA_TUNE="nsplit=N,deep=0|1".
-    if (const char* t = std::getenv("DELTA_TUNE")) {
-        const char* a = std::strstr(t, "nsplit=");
-        while (a && a != t && a[-1] != ',') a = std::strstr(a + 1, "nsplit=");  // not "snsplit="
-        const char* d = std::strstr(t, "deep=");
-        if (a) h->tune_nsplit = std::atoi(a + 7);
-        if (d) h->tune_deep = std::atoi(d + 5);
-        if (const char* w = std::strstr(t, "prewait=")) h->tune_prewait = std::atoi(w + 8);
-        if (const char* w = std::strstr(t, "snsplit=")) h->tune_snsplit = std::atoi(w + 8);
-        if (const char* w = std::strstr(t, "early=")) h->tune_early = std::atoi(w + 6);
-        if (const char* w = std::strstr(t, "umma=")) h->tune_umma = std::atoi(w + 5);
-        if (const char* w = std::strstr(t, "policy=")) h->tune_policy = std::atoi(w + 7);
-        if (const char* w = std::strstr(t, "seltrig=")) h->tune_seltrig = std::atoi(w + 8);
-        if (const char* w = std::strstr(t, "gmerge=")) h->tune_gmerge = std::atoi(w + 7);
-        if (const char* w = std::strstr(t, "selhist=")) h->tune_selhist = std::atoi(w + 8);
-        if (const char* w = std::strstr(t, "gm2=")) h->tune_gm2 = std::atoi(w + 4);
-        if (const char* w = std::strstr(t, "lat=")) h->tune_lat = std::atoi(w + 4);
-        if (const char* w = std::strstr(t, "qpf=")) h->tune_qpf = std::atoi(w + 4);
-    }
     h->step.assign(cfg->num_layers, 0);
     h->dec_step.assign(cfg->num_layers, -1);
     h->sel_step.assign(std::max(1, cfg->num_select_layers), -1);
@@ -1222,6 +1203,34 @@ const char* delta_last_error_message(delta_t h) { return h ? h->msg.c_str() : g_
 uint64_t delta_kernels_launched(delta_t h) { return h ? h->launches : 0; }
 
 uint64_t delta_graph_captures(delta_t h) { return h ? h->captures : 0; }
+
+const char* delta_layer_kernel_name(delta_t h, int32_t layer, int32_t batch) {
+    if (!h || layer < 0 || layer >= h->cfg.num_layers || batch < 1 || batch > h->cfg.max_batch) return "";
+    const AttnParams p = attn_params(h, layer, batch);
+    if (!h->use_tc) return "attn_simt_kernel (fp32, cluster split-K merge)";
+    if (h->tune_umma && umma_supported(p)) return "attn_umma_kernel (tcgen05, cluster split-K merge)";
+    if (p.sparse_lat) return "sparse_lat_kernel (resident plan tiles, cluster DSMEM split-K merge)";
+    if (p.gmerge) return "attn_tc_kernel (one CTA per SM, global split-K merge)";
+    return "attn_tc_kernel (cluster DSMEM split-K merge)";
+}
+
+delta_status delta_set_tuning(delta_t h, const char* key, int32_t value) {
+    if (!h || !key) return fail(h, DELTA_ERR_USAGE, "null handle or key");
+    struct Knob { const char* name; int* field; };
+    const Knob knobs[] = {
+        {"nsplit", &h->tune_nsplit}, {"snsplit", &h->tune_snsplit}, {"deep", &h->tune_deep},
+        {"prewait", &h->tune_prewait}, {"early", &h->tune_early}, {"umma", &h->tune_umma},
+        {"policy", &h->tune_policy}, {"seltrig", &h->tune_seltrig}, {"selhist", &h->tune_selhist},
+        {"gmerge", &h->tune_gmerge}, {"gm2", &h->tune_gm2}, {"lat", &h->tune_lat}, {"qpf", &h->tune_qpf}};
+    for (const Knob& k : knobs)
+        if (std::strcmp(k.name, key) == 0) {
+            *k.field = value;
+            for (auto& g : h->graphs)  // captured steps baked the old setting in
+                if (g.exec) { cudaGraphExecDestroy(g.exec); g.exec = nullptr; }
+            return DELTA_OK;
+        }
+    return fail(h, DELTA_ERR_CONFIG, std::string("unknown tuning key: ") + key);
+}
 
 delta_status delta_read_bandwidth_probe(const void* buf, size_t bytes, float* sink, cudaStream_t stream) {
     if (!buf || !sink) return fail(nullptr, DELTA_ERR_USAGE, "null buffer");

@@ -65,6 +65,17 @@ def main():
             assert st.get_error() == 0
             t = np.array([1e3 * ev[i].elapsed_time(ev[i + 1]) for i in range(a.steps)])
             res[name] = (np.median(t), np.percentile(t, 10), np.percentile(t, 90), t.mean())
+            if sel:  # eager select of the first Delta layer, back to back
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(s):
+                    for _ in range(5):
+                        st.select(delta[0], 1, stream=s)
+                    e0.record(s)
+                    for _ in range(50):
+                        st.select(delta[0], 1, stream=s)
+                    e1.record(s)
+                s.synchronize()
+                print(f"   [{tune}] eager select {1e3 * e0.elapsed_time(e1) / 50:.2f} us", flush=True)
         line = "  ".join(f"{n} p50 {r[0]:7.1f} p10 {r[1]:7.1f} p90 {r[2]:7.1f} mean {r[3]:7.1f} us" for n, r in res.items())
         if "full" in res:
             line += f"  speedup {res['full'][0] / res['delta'][0]:.3f}"
