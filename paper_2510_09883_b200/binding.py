@@ -285,27 +285,65 @@ class DeltaStack:
         bt = block_table.to(device=device, dtype=torch.int32).contiguous()
         return cls(cfg, kv_pool, bt, ws)
 
+    # ------------------------------------------------------------------ argument checks
+    def _arg(self, t, kind: str, shape, name: str, host: bool = False):
+        """Marshalling checks only (no arithmetic): dtype, contiguity, device and shape of a tensor
+        argument before its raw pointer crosses the C ABI (which cannot check them)."""
+        import torch
+        dt = {"kv": torch.bfloat16 if self.cfg.kv_dtype == DELTA_BF16 else torch.float32,
+              "f32": torch.float32, "i32": torch.int32}[kind]
+        if t.dtype != dt:
+            raise DeltaError(2, f"{name}: dtype {t.dtype}, expected {dt}")
+        if not t.is_contiguous():
+            raise DeltaError(2, f"{name}: must be contiguous")
+        if host:
+            if t.is_cuda:
+                raise DeltaError(2, f"{name}: must be a host tensor")
+        elif not t.is_cuda or t.device != self.kv_pool.device:
+            raise DeltaError(2, f"{name}: must live on {self.kv_pool.device}")
+        if len(t.shape) != len(shape) or any(e is not None and a != e for a, e in zip(t.shape, shape)):
+            raise DeltaError(2, f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)} (None = any)")
+        return t.data_ptr()
+
+    def _opt(self, t, kind, shape, name, host=False):
+        return None if t is None else self._arg(t, kind, shape, name, host)
+
     # ------------------------------------------------------------------ calls
     def set_seq_lens(self, lens, layer: int = -1, stream=None):
         arr = (ctypes.c_int32 * len(lens))(*[int(x) for x in lens])
         _check(self.lib.delta_set_seq_lens(self.h, layer, len(lens), arr, _stream(stream)), self.h)
 
     def append_kv(self, layer: int, k_new, v_new, stream=None):
+        c = self.cfg
         batch, ntok = k_new.shape[0], k_new.shape[1]
-        _check(self.lib.delta_append_kv(self.h, layer, batch, ntok, k_new.data_ptr(), v_new.data_ptr(),
-                                        _stream(stream)), self.h)
+        kp = self._arg(k_new, "kv", (batch, ntok, c.num_kv_heads, c.head_dim), "k_new")
+        vp_ = self._arg(v_new, "kv", (batch, ntok, c.num_kv_heads, c.head_dim), "v_new")
+        _check(self.lib.delta_append_kv(self.h, layer, batch, ntok, kp, vp_, _stream(stream)), self.h)
 
     def decode_layer(self, layer: int, q, out, lse=None, stream=None):
-        _check(self.lib.delta_decode_layer(self.h, layer, q.shape[0], q.data_ptr(), out.data_ptr(), _ptr(lse),
-                                           _stream(stream)), self.h)
+        c = self.cfg
+        b = q.shape[0]
+        qp = self._arg(q, "kv", (b, c.num_q_heads, c.head_dim), "q")
+        op = self._arg(out, "f32", (b, c.num_q_heads, c.head_dim), "out")
+        lp = self._opt(lse, "f32", (b, c.num_q_heads), "lse")
+        _check(self.lib.delta_decode_layer(self.h, layer, b, qp, op, lp, _stream(stream)), self.h)
 
     def append_decode_layer(self, layer: int, k_new, v_new, q, out, lse=None, stream=None):
-        _check(self.lib.delta_append_decode_layer(self.h, layer, q.shape[0], k_new.data_ptr(), v_new.data_ptr(),
-                                                  q.data_ptr(), out.data_ptr(), _ptr(lse), _stream(stream)), self.h)
+        c = self.cfg
+        b = q.shape[0]
+        kp = self._arg(k_new, "kv", (b, c.num_kv_heads, c.head_dim), "k_new")
+        vp_ = self._arg(v_new, "kv", (b, c.num_kv_heads, c.head_dim), "v_new")
+        qp = self._arg(q, "kv", (b, c.num_q_heads, c.head_dim), "q")
+        op = self._arg(out, "f32", (b, c.num_q_heads, c.head_dim), "out")
+        lp = self._opt(lse, "f32", (b, c.num_q_heads), "lse")
+        _check(self.lib.delta_append_decode_layer(self.h, layer, b, kp, vp_, qp, op, lp, _stream(stream)), self.h)
 
     def select(self, layer: int, batch: int, keys_override=None, idx_out=None, count_out=None, stream=None):
-        _check(self.lib.delta_select(self.h, layer, batch, _ptr(keys_override), _ptr(idx_out), _ptr(count_out),
-                                     _stream(stream)), self.h)
+        cap = self.plan_capacity
+        kp = self._opt(keys_override, "f32", (batch, None), "keys_override")
+        ip = self._opt(idx_out, "i32", (batch, cap), "idx_out")
+        cp = self._opt(count_out, "i32", (batch,), "count_out")
+        _check(self.lib.delta_select(self.h, layer, batch, kp, ip, cp, _stream(stream)), self.h)
 
     def quest_build_reps(self, layer: int = -1, batch: int | None = None, stream=None):
         _check(self.lib.delta_quest_build_reps(self.h, layer, batch or self.cfg.max_batch, _stream(stream)), self.h)
@@ -324,8 +362,14 @@ class DeltaStack:
 
     def prefill(self, layer: int, q, k_new, v_new, out, lse=None, stream=None):
         """Chunked prefill: append q.shape[1] tokens and attend causally (q [B][ntok][m][d])."""
-        _check(self.lib.delta_prefill(self.h, layer, q.shape[0], q.shape[1], q.data_ptr(), k_new.data_ptr(),
-                                      v_new.data_ptr(), out.data_ptr(), _ptr(lse), _stream(stream)), self.h)
+        c = self.cfg
+        b, n = q.shape[0], q.shape[1]
+        qp = self._arg(q, "kv", (b, n, c.num_q_heads, c.head_dim), "q")
+        kp = self._arg(k_new, "kv", (b, n, c.num_kv_heads, c.head_dim), "k_new")
+        vp_ = self._arg(v_new, "kv", (b, n, c.num_kv_heads, c.head_dim), "v_new")
+        op = self._arg(out, "f32", (b, n, c.num_q_heads, c.head_dim), "out")
+        lp = self._opt(lse, "f32", (b, n, c.num_q_heads), "lse")
+        _check(self.lib.delta_prefill(self.h, layer, b, n, qp, kp, vp_, op, lp, _stream(stream)), self.h)
 
     def workspace_region(self, which: int):
         """(device pointer, bytes) of a workspace region (0 unit keys, 1 Quest reps)."""
@@ -334,13 +378,23 @@ class DeltaStack:
         return ptr.value, n.value
 
     def decode_step(self, q_all, k_all, v_all, out_all, lse_all=None, stream=None):
-        _check(self.lib.delta_decode_step(self.h, q_all.shape[1], q_all.data_ptr(), k_all.data_ptr(),
-                                          v_all.data_ptr(), out_all.data_ptr(), _ptr(lse_all), _stream(stream)),
-               self.h)
+        c = self.cfg
+        L, b = c.num_layers, q_all.shape[1]
+        qp = self._arg(q_all, "kv", (L, b, c.num_q_heads, c.head_dim), "q_all")
+        kp = self._arg(k_all, "kv", (L, b, c.num_kv_heads, c.head_dim), "k_all")
+        vp_ = self._arg(v_all, "kv", (L, b, c.num_kv_heads, c.head_dim), "v_all")
+        op = self._arg(out_all, "f32", (L, b, c.num_q_heads, c.head_dim), "out_all")
+        lp = self._opt(lse_all, "f32", (L, b, c.num_q_heads), "lse_all")
+        _check(self.lib.delta_decode_step(self.h, b, qp, kp, vp_, op, lp, _stream(stream)), self.h)
 
     def decode_step_host(self, q_host, k_host, v_host, out_host, stream=None):
-        _check(self.lib.delta_decode_step_host(self.h, q_host.shape[1], q_host.data_ptr(), k_host.data_ptr(),
-                                               v_host.data_ptr(), out_host.data_ptr(), _stream(stream)), self.h)
+        c = self.cfg
+        L, b = c.num_layers, q_host.shape[1]
+        qp = self._arg(q_host, "kv", (L, b, c.num_q_heads, c.head_dim), "q_host", host=True)
+        kp = self._arg(k_host, "kv", (L, b, c.num_kv_heads, c.head_dim), "k_host", host=True)
+        vp_ = self._arg(v_host, "kv", (L, b, c.num_kv_heads, c.head_dim), "v_host", host=True)
+        op = self._arg(out_host, "f32", (L, b, c.num_q_heads, c.head_dim), "out_host", host=True)
+        _check(self.lib.delta_decode_step_host(self.h, b, qp, kp, vp_, op, _stream(stream)), self.h)
 
     def exchange_buffers(self, which: int):
         """(send_ptr, recv_ptr, block_bytes) of the external exchange (0: attention, 1: candidates)."""

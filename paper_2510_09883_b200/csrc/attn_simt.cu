@@ -138,12 +138,12 @@ __global__ void __launch_bounds__(NW * 32) attn_simt_kernel(const AttnParams p) 
 template <typename T, int D>
 cudaError_t launch_impl(const AttnParams& p0, cudaStream_t st, bool pdl) {
     auto kern = attn_simt_kernel<T, D>;
-    static int max_cluster = 0;
-    if (max_cluster == 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        max_cluster = cluster_limit((const void*)kern, NW * 32, 0);
-    }
+    static std::atomic<int> cache[kMaxDevices];  // per device: attribute opt-ins are per context
+    const int max_cluster = per_device_once(cache, [&] {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return -1;
+        return cluster_limit((const void*)kern, NW * 32, 0);
+    });
+    if (max_cluster < 1) return cudaErrorInvalidConfiguration;
     AttnParams p = p0;
     p.nsplit = p.nsplit < max_cluster ? p.nsplit : max_cluster;
     cudaLaunchConfig_t cfg = {};

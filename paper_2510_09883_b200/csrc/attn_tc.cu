@@ -494,13 +494,15 @@ cudaError_t launch_impl(const AttnParams& p0, const CUtensorMap* tm_kv,
     auto kern = attn_tc_kernel<D, TOKEN_PLAN, NST, NH, NG, CL>;
     constexpr int kThreads = cta_threads<NG>();
     constexpr int smem = TcCfg<D, NST>::kSmem;
-    static int max_cluster = 0;  // largest feasible cluster for this instantiation
-    if (max_cluster == 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e == cudaSuccess && CL) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        max_cluster = CL ? cluster_limit((const void*)kern, kThreads, smem) : kMaxSplitG;
-    }
+    // largest feasible cluster for this instantiation, per device (attribute opt-ins are per context)
+    static std::atomic<int> cache[kMaxDevices];
+    const int max_cluster = per_device_once(cache, [&] {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+            (CL && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess))
+            return -1;
+        return CL ? cluster_limit((const void*)kern, kThreads, smem) : kMaxSplitG;
+    });
+    if (max_cluster < 1) return cudaErrorInvalidConfiguration;
     AttnParams p = p0;
     p.nsplit = std::min(p.nsplit, max_cluster);
     cudaLaunchConfig_t cfg = {};

@@ -486,13 +486,14 @@ template <int D, bool TOKEN_PLAN, int NR>
 cudaError_t launch_impl(const AttnParams& p0, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl) {
     auto kern = attn_umma_kernel<D, TOKEN_PLAN, NR>;
     constexpr int smem = UCfg<D, NR>::kSmem;
-    static int max_cluster = 0;
-    if (max_cluster == 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        max_cluster = cluster_limit((const void*)kern, kUThreads, smem);
-    }
+    static std::atomic<int> cache[kMaxDevices];  // per device: attribute opt-ins are per context
+    const int max_cluster = per_device_once(cache, [&] {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+            cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+            return -1;
+        return cluster_limit((const void*)kern, kUThreads, smem);
+    });
+    if (max_cluster < 1) return cudaErrorInvalidConfiguration;
     AttnParams p = p0;
     p.nsplit = std::min(p.nsplit, max_cluster);
     cudaLaunchConfig_t cfg = {};

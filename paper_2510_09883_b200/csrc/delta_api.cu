@@ -116,6 +116,9 @@ std::string validate(const delta_config& c, std::vector<int>& role, std::vector<
         if (c.select_block != c.page_size) return "QUEST / RAAS work on pages: select_block must be page_size";
         if (c.kv_dtype != DELTA_BF16) return "QUEST / RAAS need bf16 KV";
         if (c.shard_world != 1) return "QUEST / RAAS are not sequence-sharded";
+        // raas_update stages 16 B per page of a sequence in shared memory (opt-in limit 200 KiB)
+        if (c.policy == DELTA_POLICY_RAAS && 16LL * ((c.max_seq_len + kPage - 1) / kPage + 1) > 200 * 1024)
+            return "RAAS: max_seq_len too large for the eviction kernel's shared memory (<= 204,784 tokens)";
         role.assign(c.num_layers, c.policy == DELTA_POLICY_QUEST ? kRoleQuest : kRoleRaas);
         gov.assign(c.num_layers, 0);
         for (int l = 0; l < c.num_layers; ++l) {
@@ -511,8 +514,12 @@ delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_ov
 // page is a forced window page), then one launch that appends the token (pool rows, reps,
 // length) and ranks the pages -> plan slot 0.
 delta_status launch_quest_select(delta_ctx* h, int layer, int batch, const void* k_new, const void* v_new,
-                                 const void* q, cudaStream_t st) {
-    cudaError_t e = launch_quest_score(quest_params(h, layer, batch, q), h->L.max_pages, h->sms, st, h->pdl);
+                                 const void* q, cudaStream_t st, bool in_step) {
+    QuestParams qp = quest_params(h, layer, batch, q);
+    // early reads only inside a captured step, and only if the previous kernel is another
+    // layer's (an append, attention or reps rebuild of this layer writes its counter / reps)
+    qp.prewait = (in_step && h->tune_prewait && h->last_kind != delta_ctx::kLastNone && h->last_layer != layer) ? 1 : 0;
+    cudaError_t e = launch_quest_score(qp, h->L.max_pages, h->sms, st, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "quest score launch");
     ++h->launches;
     return launch_sel(h, layer, batch, h->at<float>(h->L.keys), nullptr, nullptr, st, 0, k_new, v_new);
@@ -541,7 +548,7 @@ RaasParams raas_params(delta_ctx* h, int layer, int batch) {
 delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new, const void* v_new,
                            const void* q, float* out, float* lse_out, cudaStream_t st, bool in_step = false) {
     if (h->role[layer] == kRoleQuest) {
-        delta_status s = launch_quest_select(h, layer, batch, k_new, v_new, q, st);
+        delta_status s = launch_quest_select(h, layer, batch, k_new, v_new, q, st, in_step);
         if (s != DELTA_OK) return s;
         k_new = v_new = nullptr;  // appended above
     }

@@ -168,6 +168,7 @@ struct QuestParams {
     const int32_t* seq_len;     // raw counters n * g
     const void* q;              // [batch][m][d] bf16
     float* keys;                // [max_batch][max_units] page keys
+    int prewait;                // 1: length counter and reps read before griddepcontrol.wait (see quest.cu)
 };
 cudaError_t launch_quest_reps(const QuestParams& p, int max_pages, cudaStream_t st, bool pdl);
 cudaError_t launch_quest_score(const QuestParams& p, int max_pages, int sms, cudaStream_t st, bool pdl);

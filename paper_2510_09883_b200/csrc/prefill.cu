@@ -239,13 +239,14 @@ cudaError_t launch_prefill(const PrefillParams& p, cudaStream_t st, bool pdl) {
                    : p.d == 64  ? (big ? (const void*)prefill_kernel<64, 32> : (const void*)prefill_kernel<64, 16>)
                                 : nullptr;
     if (!fn) return cudaErrorInvalidValue;
-    static const void* configured[4] = {};
-    const int slot = (p.d == 128 ? 0 : 2) + (big ? 1 : 0);
-    if (configured[slot] != fn) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)std::max(prefill_smem_bytes(128, 8), prefill_smem_bytes(128, kMaxGs)));
+    static std::atomic<int> cache[kMaxDevices * 4];  // per (device, instantiation)
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+    const int slot = dev * 4 + (p.d == 128 ? 0 : 2) + (big ? 1 : 0);
+    if (cache[slot].load(std::memory_order_acquire) == 0) {  // opt in to the dynamic shared memory
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max(prefill_smem_bytes(128, 8), prefill_smem_bytes(128, kMaxGs)));
         if (e != cudaSuccess) return e;
-        configured[slot] = fn;
+        cache[slot].store(1, std::memory_order_release);
     }
     void* args[] = {const_cast<PrefillParams*>(&p)};
     return cudaLaunchKernelExC(&cfg, fn, args);

@@ -50,9 +50,11 @@ __global__ void __launch_bounds__(256) quest_score_kernel(const QuestParams p) {
     using Vec = typename std::conditional<E == 4, uint2, uint32_t>::type;  // E bf16
     extern __shared__ float sq[];  // [m][D]
     const int b = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // Before the dependency wait: the length counter, block table and this layer's reps are not
-    // written by the preceding kernels of a step (only q is), so the first page's reps stream in
-    // while the previous kernel finishes.
+    // With `prewait` (set by the host only inside a captured step, when the previous kernel is
+    // another layer's: it wrote neither this layer's length counter nor its reps) the length and
+    // the first page's reps stream in before the dependency wait; otherwise (eager calls, e.g.
+    // delta_append_kv of this layer right before) everything is read after it.
+    if (!p.prewait) pdl_wait();
     const int n = p.seq_len[p.layer * p.max_batch + b] / p.g;
     const int n_pages = (n + kPage - 1) / kPage;
     const int gs = p.m / p.g;
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(256) quest_score_kernel(const QuestParams p) {
     Vec vmn[G], vmx[G];
     int u = blockIdx.x * 8 + warp;
     if (u < n_pages) load_reps(u, vmn, vmx);
-    pdl_wait();
+    if (p.prewait) pdl_wait();
     pdl_launch_dependents();
     {   // 16-byte loads of q (all issued before the first store)
         const uint4* q8 = reinterpret_cast<const uint4*>(p.q) + (size_t)b * p.m * D / 8;
@@ -155,12 +157,14 @@ cudaError_t launch_quest_score(const QuestParams& p, int max_pages, int sms, cud
                    : p.d == 64  ? (p.g <= 8 ? (const void*)quest_score_kernel<64, 8> : (const void*)quest_score_kernel<64, 16>)
                                 : nullptr;
     if (!fn) return cudaErrorInvalidValue;
-    static const void* configured[4] = {};
-    const int slot = (p.d == 128 ? 0 : 2) + (p.g <= 8 ? 0 : 1);
-    if (configured[slot] != fn) {  // opt in to > 48 KiB of staged q (m * d fp32, m <= 256)
+    static std::atomic<int> cache[kMaxDevices * 4];  // per (device, instantiation)
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+    const int slot = dev * 4 + (p.d == 128 ? 0 : 2) + (p.g <= 8 ? 0 : 1);
+    if (cache[slot].load(std::memory_order_acquire) == 0) {  // opt in to the dynamic shared memory
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 128 * 4);
         if (e != cudaSuccess) return e;
-        configured[slot] = fn;
+        cache[slot].store(1, std::memory_order_release);
     }
     void* args[] = {const_cast<QuestParams*>(&p)};
     return cudaLaunchKernelExC(&cfg, fn, args);

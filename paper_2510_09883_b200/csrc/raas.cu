@@ -207,13 +207,12 @@ cudaError_t launch_raas_update(const RaasParams& p, cudaStream_t st, bool pdl) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(raas_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             200 * 1024);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<int> cache[kMaxDevices];  // per device: attribute opt-ins are per context
+    if (per_device_once(cache, [] {
+            return cudaFuncSetAttribute(raas_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ==
+                           cudaSuccess ? 1 : -1;
+        }) < 0)
+        return cudaErrorInvalidConfiguration;
     return cudaLaunchKernelEx(&cfg, raas_update_kernel, p);
 }
 

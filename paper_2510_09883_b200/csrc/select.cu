@@ -686,13 +686,13 @@ size_t select_smem_bytes(int max_units) {
 
 cudaError_t launch_select(const SelectParams& p, cudaStream_t st, bool pdl) {
     const size_t smem = select_smem_bytes(p.max_units);
-    static bool configured = false;  // static + dynamic shared memory exceeds the 48 KiB default
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(2 * kSmemUnits * sizeof(uint32_t)));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    // static + dynamic shared memory exceeds the 48 KiB default; opt in once per device
+    static std::atomic<int> cache[kMaxDevices];
+    if (per_device_once(cache, [] {
+            return cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(2 * kSmemUnits * sizeof(uint32_t))) == cudaSuccess ? 1 : -1;
+        }) < 0)
+        return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.keys_override ? 1 : p.nchunk, p.batch);
     cfg.blockDim = dim3(kSelThreads);

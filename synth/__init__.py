@@ -27,6 +27,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 M64 = (1 << 64) - 1
@@ -60,8 +62,27 @@ def stream_key(seed: int, tag: int, layer: int = 0, seq: int = 0, step: int = 0)
 
 
 def normal_f32(key: int, idx: np.ndarray) -> np.ndarray:
-    """Irwin-Hall(12) approx N(0,1), exact multiples of 2**-16, as float32."""
-    idx = idx.astype(np.uint64)
+    """Irwin-Hall(12) approx N(0,1), exact multiples of 2**-16, as float32.  Large requests are
+    split into chunks evaluated on a thread pool (numpy releases the GIL; the values are the same
+    element by element)."""
+    idx = np.asarray(idx).astype(np.uint64)
+    if idx.size >= (1 << 21):
+        from concurrent.futures import ThreadPoolExecutor
+        flat = idx.reshape(-1)
+        nchunk = min(32, max(1, (os.cpu_count() or 1) * 2))
+        bounds = np.linspace(0, flat.size, nchunk + 1).astype(np.int64)
+        out = np.empty(flat.size, np.float32)
+
+        def work(i):
+            out[bounds[i]:bounds[i + 1]] = _normal_f32(key, flat[bounds[i]:bounds[i + 1]])
+
+        with ThreadPoolExecutor(max_workers=nchunk) as ex:
+            list(ex.map(work, range(nchunk)))
+        return out.reshape(idx.shape)
+    return _normal_f32(key, idx)
+
+
+def _normal_f32(key: int, idx: np.ndarray) -> np.ndarray:
     base = np.uint64(key)
     with np.errstate(over="ignore"):
         S = np.zeros(idx.shape, np.int64)

@@ -8,7 +8,7 @@ import pytest
 import oracle
 import synth
 from helpers import (C0, C0_PAGE, C1, GpuCase, Shape, assert_close_bf16, assert_close_fp32, check_plan,
-                     oracle_step, planting_for)
+                     oracle_layer, oracle_step, planting_for)
 
 pytestmark = pytest.mark.gpu
 
@@ -36,7 +36,10 @@ def _check_step(case: GpuCase, s: int, out, lse, plans, layers=None, exact_plans
             if layers is not None and l not in layers:
                 continue
             if roles[l] == oracle.ROLE_SPARSE and not same_plan.get(int(gov[l]), True):
-                continue  # near-tie swap at the boundary (R20 iii): outputs legitimately differ
+                # near-tie swap at the boundary (R20 iii): the GPU attended its own (valid) plan,
+                # so its output is checked against the oracle attending that plan
+                toks = oracle.units_to_tokens(np.asarray(plans[int(gov[l])][b]), sh.block, s)
+                o_out, o_lse, _ = oracle_layer(sh, case.seed, l, b, s, case.planting, tokens=toks)
             _cmp(sh, out[l, b], o_out, f"layer {l} seq {b}")
             assert np.max(np.abs(lse[l, b] - o_lse)) <= _lse_tol(sh), f"lse layer {l}"
 
@@ -298,9 +301,83 @@ def test_c1_full_size_planted_graph_step():
     for l in layers:
         assert_close_bf16(out[l, 0], ref[l][0], f"C1 layer {l}")
         assert np.max(np.abs(lse[l, 0] - ref[l][1])) <= 2e-4
-    # Delta selections: known without the oracle
-    units = set(synth.planted_units(2511, 2, 0, plant).tolist())
-    assert set(ref[2][2].tolist()) == units | {0, 2046, 2047}   # sink page + 2 window pages
+    # Delta selections: known without the oracle, and the GPU's plans equal them
+    for dl in C1.delta:
+        units = set(synth.planted_units(2511, dl, 0, plant).tolist())
+        expect = units | {0, 2046, 2047}                          # sink page + 2 window pages
+        assert set(ref[dl][2].tolist()) == expect, f"oracle plan layer {dl}"
+        assert set(_gpu_plan(case, dl, 1)[0].tolist()) == expect, f"GPU plan layer {dl}"
+
+
+# ---------------------------------------------------------------- the other configs at full size
+
+def _gpu_plan(case: GpuCase, layer: int, batch: int):
+    cap = case.stack.plan_capacity
+    idx = torch.empty((batch, cap), dtype=torch.int32, device="cuda")
+    cnt = torch.empty((batch,), dtype=torch.int32, device="cuda")
+    case.stack.copy_plan(layer, batch, idx, cnt)
+    torch.cuda.synchronize()
+    return [idx[b, : int(cnt[b])].cpu().numpy() for b in range(batch)]
+
+
+def _gpu_keys(case: GpuCase):
+    ptr, n = case.stack.workspace_region(0)
+    ws = case.stack.workspace
+    off = ptr - ws.data_ptr()
+    return ws[off: off + n].view(torch.float32).view(case.cfg.max_batch, -1).cpu().numpy()
+
+
+def _full_size_sampled(shape: Shape, batch: int, s: int, seqs, layers, seed: int):
+    """One graph-captured step at the config's full size and batch, in the launch configuration
+    bench.py times (its split counts, merge variants and kernels), on iid inputs; sampled
+    (sequence, layer) outputs against the oracle (R19; a sparse layer whose governing plan differs
+    from the oracle's only near the boundary is checked against the oracle on the GPU's plan,
+    R20 iii), the plans of the sampled sequences (R20 iii), and the last Delta layer's unit keys
+    within 1e-5 relative of the oracle's exact S_u (R20 ii)."""
+    case = GpuCase(shape, seed, batch=batch, s_pre=s - 1, max_seq=s + 32)
+    out, lse = case.step_graph(s)
+    assert case.stack.get_error() == 0
+    keys = _gpu_keys(case)
+    plans = {dl: _gpu_plan(case, dl, batch) for dl in shape.delta}
+    roles, gov = oracle.validate_tiers(shape.L, shape.F, shape.delta)
+    n_units = -(-s // shape.block)
+    for b in seqs:
+        ref = oracle_step(shape, seed, b, s, layers + [shape.delta[-1]])
+        same = {dl: check_plan(plans[dl][b], ref[dl][2], ref[dl][3], s, shape, False) for dl in ref if ref[dl][2] is not None}
+        for l in layers:
+            o_out, o_lse = ref[l][0], ref[l][1]
+            if roles[l] == oracle.ROLE_SPARSE and not same[int(gov[l])]:
+                toks = oracle.units_to_tokens(plans[int(gov[l])][b], shape.block, s)
+                o_out, o_lse, _ = oracle_layer(shape, seed, l, b, s, tokens=toks)
+            assert_close_bf16(out[l, b], o_out, f"layer {l} seq {b}")
+            assert np.max(np.abs(lse[l, b] - o_lse)) <= 2e-4, f"lse layer {l} seq {b}"
+        o_keys = ref[shape.delta[-1]][3][:n_units]
+        g_keys = keys[b, :n_units].astype(np.float64)
+        live = o_keys > 1e-30
+        rel = np.abs(g_keys - o_keys)[live] / o_keys[live]
+        assert rel.max() <= 1e-5, f"unit keys seq {b}: max rel {rel.max():.3g}"
+    del case
+    torch.cuda.empty_cache()
+
+
+C2 = Shape(L=28, m=28, g=4, d=128, F=2, delta=[2, 14, 22], k=4096, S=4, Lw=32, block=16, dtype="bf16")
+C4 = Shape(L=40, m=40, g=8, d=128, F=2, delta=[2, 6, 35], k=2048, S=4, Lw=32, block=16, dtype="bf16")
+
+
+def test_c2_full_size_sampled():
+    """BASELINE configs[2] per GPU at W=1: Qwen-7B shape, b=32, 16K context, budget 4K (B*g = 128:
+    one global-merge split per (sequence, head) on the full-cache layers, cluster kernel sparse)."""
+    _full_size_sampled(C2, 32, 16384, seqs=[0, 13, 31], layers=[0, 2, 3, 14, 21, 27], seed=2512)
+
+
+def test_c4_full_size_sampled():
+    """BASELINE configs[4] per GPU: Qwen3-14B shape, 8 sequences at 32K, budget 2K (B*g = 64)."""
+    _full_size_sampled(C4, 8, 32768, seqs=[0, 7], layers=[1, 6, 7, 35, 39], seed=2514)
+
+
+def test_c3_full_size_sampled():
+    """BASELINE configs[3] on one GPU: Llama-8B shape at 128K context (8192 pages), budget 2K."""
+    _full_size_sampled(C1, 1, 131072, seqs=[0], layers=[0, 2, 3, 25, 26, 31], seed=2513)
 
 
 # ---------------------------------------------------------------- tcgen05 / TMEM kernel (opt-in)

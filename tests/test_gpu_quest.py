@@ -221,3 +221,36 @@ def test_quest_reps_after_prefill_chunk():
     out, lse, plans, keys = case.step(s)
     _check_reps(case, s)
     _check_layer(case, s, out, lse, plans, keys)
+
+
+def test_quest_append_then_decode_scores_the_new_pages():
+    """delta_append_kv of more tokens than the window, then an immediate Quest
+    delta_decode_layer (no fused append).  The score kernel must read the length counter and the
+    representatives after the append completed (no pre-wait reads outside a captured step): every
+    page the append opened gets its exact key, and plan and outputs match the oracle."""
+    shape, seed, n0, ntok = QUEST_SMALL, 59, 2000, 100   # 100 > n_window = 32: new non-window pages
+    case = QuestCase(shape, seed, batch=1, s_pre=n0, max_seq=n0 + ntok + 64)
+    s = n0 + ntok
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).cuda()  # noqa: E731
+    out = torch.empty((shape.L, 1, shape.m, shape.d), dtype=torch.float32, device="cuda")
+    lse = torch.empty((shape.L, 1, shape.m), dtype=torch.float32, device="cuda")
+    cap = case.stack.plan_capacity
+    plans, keys = {}, {}
+    for l in range(shape.L):
+        kn = synth.kv_rows(seed, l, 0, n0, s, shape.g, shape.d, "bf16", "k")[None]
+        vn = synth.kv_rows(seed, l, 0, n0, s, shape.g, shape.d, "bf16", "v")[None]
+        case.stack.append_kv(l, to(kn), to(vn))
+        q = to(synth.q_rows(seed, l, 0, s, shape.m, shape.d, "bf16")[None])
+        case.stack.decode_layer(l, q, out[l], lse[l])
+        if l >= shape.F:
+            idx = torch.empty((1, cap), dtype=torch.int32, device="cuda")
+            cnt = torch.empty((1,), dtype=torch.int32, device="cuda")
+            case.stack.copy_plan(l, 1, idx, cnt)
+            keys[l] = case.keys()
+            plans[l] = (idx, cnt)
+    torch.cuda.synchronize()
+    assert case.stack.get_error() == 0
+    hp = {l: [idx[0, : int(cnt[0])].cpu().numpy()] for l, (idx, cnt) in plans.items()}
+    hk = {l: kk.cpu().numpy() for l, kk in keys.items()}
+    _check_reps(case, s)
+    _check_layer(case, s, out.cpu().numpy(), lse.cpu().numpy(), hp, hk)
