@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -23,6 +24,27 @@ using namespace delta;
 namespace {
 
 thread_local std::string g_msg;
+
+// NVTX range per enqueued layer role (header-only NVTX v3: a no-op unless a profiler injects
+// itself), so nsys / ncu timelines of eager calls and graph captures show layer and role.
+struct NvtxRange {
+    explicit NvtxRange(const char* role, int layer) {
+        char buf[48];
+        snprintf(buf, sizeof buf, "delta L%d %s", layer, role);
+        nvtxRangePushA(buf);
+    }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+const char* role_name(int r) {
+    switch (r) {
+        case kRoleFull: return "FULL";
+        case kRoleSelect: return "SELECT";
+        case kRoleSparse: return "SPARSE";
+        case kRoleQuest: return "QUEST";
+        case kRoleRaas: return "RAAS";
+        default: return "?";
+    }
+}
 
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -547,6 +569,7 @@ RaasParams raas_params(delta_ctx* h, int layer, int batch) {
 
 delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new, const void* v_new,
                            const void* q, float* out, float* lse_out, cudaStream_t st, bool in_step = false) {
+    NvtxRange nv(role_name(h->role[layer]), layer);
     if (h->role[layer] == kRoleQuest) {
         delta_status s = launch_quest_select(h, layer, batch, k_new, v_new, q, st, in_step);
         if (s != DELTA_OK) return s;
@@ -595,6 +618,7 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
 
 delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_override, int32_t* idx_out,
                         int32_t* count_out, cudaStream_t st, int shard_mode, const void* k_new, const void* v_new) {
+    NvtxRange nv(k_new ? "QUEST select+append" : "score+top-k", layer);
     const delta_config& c = h->cfg;
     SelectParams p = {};
     p.k_new = k_new; p.v_new = v_new; p.kv_pool = h->kv_pool; p.reps = h->ws + h->L.reps;

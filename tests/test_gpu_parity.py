@@ -477,3 +477,41 @@ def test_gs16_two_head_tiles():
     case = GpuCase(shape, 95, batch=2, s_pre=1500, max_seq=1600)
     out, lse, plans = case.step_layers(1501)
     _check_step(case, 1501, out, lse, plans)
+
+
+# ---------------------------------------------------------------- numeric error flag
+
+@pytest.mark.parametrize("where", ["sparse_q", "full_q", "select_cache"])
+def test_injected_nan_sets_sticky_numeric_error(where):
+    """A NaN in a layer's query (SPARSE: the latency kernel; FULL: the global-merge kernel) or in
+    a cached key row of the Delta layer makes that layer's outputs NaN, and the graph-captured step
+    raises the sticky DELTA_ERR_NUMERIC flag; delta_get_error reads and clears it, and
+    the next clean step leaves it clear."""
+    shape = Shape(L=4, m=32, g=8, d=128, F=1, delta=[1], k=512, S=4, Lw=32, block=16, dtype="bf16")
+    case = GpuCase(shape, 61, batch=1, s_pre=2999, max_seq=3100)
+    assert "sparse_lat" in case.stack.kernel_name(3, 1) and "global" in case.stack.kernel_name(0, 1)
+    q, k, v = case.inputs(3000)
+    if where == "sparse_q":
+        q[3, 0, 5, 7] = float("nan")
+    elif where == "full_q":
+        q[0, 0, 9, 3] = float("nan")
+    else:  # layer 1 (Delta), page 10's physical page, head 2, K row 4
+        phys = int(case.stack.block_table[0, 10])
+        case.stack.kv_pool[1, phys, 2, 0, 4, 11] = float("nan")
+    out = torch.empty((4, 1, 32, 128), dtype=torch.float32, device="cuda")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        case.stack.decode_step(q, k, v, out, stream=st)
+    st.synchronize()
+    assert case.stack.get_error(stream=st) == 3                       # DELTA_ERR_NUMERIC
+    bad_layer = {"sparse_q": 3, "full_q": 0, "select_cache": 1}[where]
+    assert torch.isnan(out[bad_layer]).any()
+    assert case.stack.get_error(stream=st) == 0                       # read clears it
+    q2, k2, v2 = case.inputs(3001)
+    if where == "select_cache":
+        case.stack.kv_pool[1, phys, 2, 0, 4, 11] = 0.0
+    with torch.cuda.stream(st):
+        case.stack.decode_step(q2, k2, v2, out, stream=st)
+    st.synchronize()
+    assert case.stack.get_error(stream=st) == 0
+    assert not torch.isnan(out).any()

@@ -2,7 +2,10 @@
 RS1-RS4) over a multi-step run against the oracle's per-layer simulation on the same seeded
 inputs: every step's attended page set, the page scores (within 1e-5 relative), the eviction
 decisions (the oracle replays the GPU's fp32 scores and threshold: exact), and the outputs
-(bf16 tolerance); evicted pages never return, sink and recency pages are never evicted."""
+(bf16 tolerance); evicted pages never return, sink and recency pages are never evicted.  Beside
+the replay, the oracle's OWN fp64 trajectory (its scores, the exact threshold P/|attended|) must
+give the identical retained set at every step where no refresh comparison lies within 1e-5 of
+the threshold (R20 iii for RaaS); at a near-threshold step it is re-synchronised to the replay."""
 import numpy as np
 import pytest
 
@@ -43,6 +46,8 @@ def test_raas_multi_step_parity(batch):
     ws = st.workspace
     keys = ws[ptr - ws.data_ptr(): ptr - ws.data_ptr() + nbytes].view(torch.float32).view(batch, -1)
     evicted_total = [set() for _ in range(batch)]
+    own_ret, own_last = retained.copy(), last.copy()   # the oracle's own fp64 trajectory
+    own_checked = own_near = 0
     for s in range(n0 + 1, n0 + steps + 1):
         q = torch.empty((shape.L, batch, shape.m, shape.d), dtype=torch.bfloat16, device="cuda")
         k = torch.empty((shape.L, batch, shape.g, shape.d), dtype=torch.bfloat16, device="cuda")
@@ -78,11 +83,28 @@ def test_raas_multi_step_parity(batch):
                 last_b[s // P] = s + 1
                 exp_plan.append(s // P)
             assert g_plan.tolist() == exp_plan, f"retained set step {s} seq {b}: gpu {g_plan.tolist()} oracle {exp_plan}"
+            # the oracle's own trajectory: fp64 scores, exact threshold
+            o_ret, o_last = own_ret[b], own_last[b]
+            _, _, o_pages, o_S, _ = oracle.raas_layer_step(ocfg, kv, qo, s, o_ret, o_last)
+            thr = P / oracle.units_to_tokens(o_pages, P, s).size
+            margin = np.min(np.abs(o_S[o_pages] - thr)) / thr
+            own_plan = np.nonzero(o_ret[:n_pages])[0].tolist()
+            if s % P == 0:
+                o_ret[s // P] = 1
+                o_last[s // P] = s + 1
+                own_plan.append(s // P)
+            if margin > 1e-5:
+                assert own_plan == g_plan.tolist(), f"oracle's own trajectory differs at step {s} seq {b}"
+                own_checked += 1
+            else:                              # a refresh decision at the fp32/fp64 boundary
+                own_near += 1
+                own_ret[b], own_last[b] = ret_b.copy(), last_b.copy()
             ex = oracle.raas_exempt(n_pages, s, P, shape.S, shape.Lw)
             assert not any(ex[u] for u in ev), "an exempt page was evicted"
             evicted_total[b] |= set(ev.tolist())
             assert not (evicted_total[b] & set(g_plan.tolist())), "an evicted page came back"
             assert int(sum(1 for u in g_plan if u < n_pages and not ex[u])) <= shape.k // P
     assert st.get_error() == 0
+    assert own_checked >= 0.8 * steps * batch, f"own-trajectory checks {own_checked}, near-threshold {own_near}"
     for b in range(batch):                    # the initial set shrank to the budget
         assert len(evicted_total[b]) >= -(-n0 // P) - (shape.k // P) - 4

@@ -521,3 +521,59 @@ def test_raas_invariants_random():
         assert int(((retained > 0) & (ex == 0)).sum()) <= cap
         gone |= set(ev.tolist())
         assert not any(retained[u] for u in gone)
+
+
+def test_raas_exempt_pages():
+    """RS4 by hand: sink pages overlap [0, S), recency pages overlap [s - L, s)."""
+    assert oracle.raas_exempt(10, 150, 16, 4, 32).tolist() == [1, 0, 0, 0, 0, 0, 0, 1, 1, 1]  # 118 // 16 = 7
+    assert oracle.raas_exempt(3, 40, 16, 0, 32).tolist() == [1, 1, 1]          # window [8, 40) covers all
+    assert oracle.raas_exempt(5, 80, 16, 20, 0).tolist() == [1, 1, 0, 0, 0]   # sink [0, 20): pages 0, 1
+    assert oracle.raas_exempt(6, 96, 16, 0, 0).tolist() == [0] * 6
+    assert oracle.raas_exempt(0, 0, 16, 4, 32).tolist() == []
+
+
+def test_raas_layer_step_hand_trajectory():
+    """raas_layer_step composition (RS1-RS4) on a tiny sequence whose attention weights are known
+    by hand: m = g = d = 1, scale 1, q = [1], K_t = [ln w_t] so alpha_t = w_t / sum(w) over the
+    ATTENDED tokens; P = 2, no sink, window L = 2, budget 2 tokens (1 page).  Tokens 2, 3 (page 1)
+    weigh 4, every other token 1; V_t = [t].  Start (reset): pages 0-2 retained, last = 0.
+      s=7 : token 6 opens page 3 (last 7); attended 0..6, W = 13, S = [2, 8, 2, 1] / 13,
+            threshold P/7: page 1 refreshed (last 7); exempt {2, 3}; non-exempt {0, 1}: evict 0
+      s=8 : attended 2..7, W = 12, S = [0, 8, 2, 2] / 12, threshold 2/6: page 1 refreshed;
+            exempt {3}; non-exempt {1 (last 8), 2 (last 0)}: evict 2
+      s=9 : token 8 opens page 4; attended {2,3,6,7,8}, W = 11, S1 = 8/11, S3 = 2/11, S4 = 1/11;
+            threshold 2/5: page 1 refreshed; exempt {3, 4}; nothing to evict
+      s=10: attended {2,3,6,7,8,9}, W = 12, S1 = 8/12, S3 = S4 = 2/12; exempt {4};
+            non-exempt {1 (last 10), 3 (last 7)}: evict 3
+      s=11: token 10 opens page 5; attended {2,3,8,9,10}, W = 11; exempt {4, 5}; nothing evicted
+    Output = sum_t w_t t / W over the attended tokens (closed form)."""
+    P, smax = 2, 11
+    w = np.ones(smax)
+    w[2:4] = 4.0
+    K = np.log(w).astype(np.float32).reshape(smax, 1, 1)
+    V = np.arange(smax, dtype=np.float32).reshape(smax, 1, 1)
+    cfg = oracle.StackConfig(num_layers=1, m=1, g=1, d=1, page_size=P, num_full_prefix=0, select_layers=[],
+                             budget_k=2, n_sink=0, n_window=2, select_block=P, scale=1.0)
+    q = np.ones((1, 1), np.float32)
+    retained = np.zeros(8, np.uint8)
+    retained[:3] = 1
+    last = np.zeros(8, np.int64)
+    expect = {  # s: (attended pages, page scores by page, evicted, retained after)
+        7: ([0, 1, 2, 3], {0: 2 / 13, 1: 8 / 13, 2: 2 / 13, 3: 1 / 13}, [0], [1, 2, 3]),
+        8: ([1, 2, 3], {0: 0.0, 1: 8 / 12, 2: 2 / 12, 3: 2 / 12}, [2], [1, 3]),
+        9: ([1, 3, 4], {1: 8 / 11, 2: 0.0, 3: 2 / 11, 4: 1 / 11}, [], [1, 3, 4]),
+        10: ([1, 3, 4], {1: 8 / 12, 3: 2 / 12, 4: 2 / 12}, [3], [1, 4]),
+        11: ([1, 4, 5], {1: 8 / 11, 4: 2 / 11, 5: 1 / 11}, [], [1, 4, 5]),
+    }
+    for s in range(7, 12):
+        kv = oracle.SeqKV.from_contiguous(K[:s], V[:s], P)
+        out, lse, pages, S, ev = oracle.raas_layer_step(cfg, kv, q, s, retained, last)
+        att, sc, e_ev, e_ret = expect[s]
+        assert pages.tolist() == att, f"attended pages at s={s}"
+        for u, v in sc.items():
+            assert abs(S[u] - v) <= 1e-6, f"S[{u}] at s={s}: {S[u]} vs {v}"
+        assert ev.tolist() == e_ev, f"evicted at s={s}"
+        assert np.nonzero(retained)[0].tolist() == e_ret, f"retained after s={s}"
+        toks = oracle.units_to_tokens(np.array(att), P, s)
+        assert abs(out[0, 0] - (w[toks] * toks).sum() / w[toks].sum()) <= 1e-6
+    assert last[1] == 11 and last[3] == 7 and last[4] == 9 and last[5] == 11
