@@ -276,16 +276,18 @@ __device__ __forceinline__ void sp_epilogue(const AttnParams& p, const float* ms
     SPTRACE(12);
     SPCLK(10);
     // 2. owner merge: one thread per owned float4, ranks in ascending order
+    // only the threads that merge wait on the staging barrier (the others exit)
 #ifdef EXP_NOEPI
     if (false) {
 #else
-    if (ns > 1 && mine.n4 > 0) {
+    if (ns > 1 && tid < mine.n4) {
 #endif
         mbar_wait(bar, 0);
         SPTRACE(13);
         SPCLK(11);
         const float2* sML = reinterpret_cast<const float2*>(sM);
-        for (int k = tid; k < mine.n4; k += nthreads) {
+        {
+            const int k = tid;
             const int idx = rank * per + k, row = idx / C4, c4 = idx - row * C4;
             float2 ml[kMaxSplit];
             float4 xo[kMaxSplit];
