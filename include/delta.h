@@ -263,6 +263,9 @@ delta_status delta_get_error(delta_t h, cudaStream_t stream, delta_status* stick
  * Rank 0 calls delta_nccl_get_unique_id; the 128 bytes are broadcast to all ranks (e.g. with
  * torch.distributed) and passed as delta_config.nccl_id.  NCCL is loaded at run time
  * (libnccl.so.2 already in the process, else $DELTA_NCCL_LIB).  DELTA_ERR_NCCL if absent. */
+/* Where to dlopen NCCL from if no libnccl.so.2 is loaded or on the loader path (e.g. the copy
+ * torch ships); call before the first NCCL use.  The library reads no environment variables. */
+delta_status delta_set_nccl_library(const char* path);
 delta_status delta_nccl_get_unique_id(void* out_128_bytes);
 
 /* Host-only: the page range [*page_lo, *page_hi) of every sequence that rank cfg->shard_rank

@@ -103,6 +103,8 @@ def load_library() -> ctypes.CDLL:
     L.delta_graph_captures.restype = ctypes.c_uint64
     L.delta_read_bandwidth_probe.argtypes = [vp, ctypes.c_size_t, vp, vp]
     L.delta_read_bandwidth_probe.restype = st
+    L.delta_set_nccl_library.argtypes = [ctypes.c_char_p]
+    L.delta_set_nccl_library.restype = st
     L.delta_nccl_get_unique_id.argtypes = [vp]
     L.delta_nccl_get_unique_id.restype = st
     L.delta_shard_range.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(i32), ctypes.POINTER(i32)]
@@ -197,12 +199,12 @@ def query_sizes(cfg: DeltaConfig) -> tuple[int, int]:
 def nccl_unique_id() -> bytes:
     """128-byte ncclUniqueId from rank 0 (to broadcast with torch.distributed)."""
     import os
-    if "DELTA_NCCL_LIB" not in os.environ:
-        try:
-            import nvidia.nccl  # the copy torch uses
-            os.environ["DELTA_NCCL_LIB"] = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
-        except Exception:  # noqa: BLE001
-            pass
+    try:
+        import nvidia.nccl  # the copy torch uses
+        path = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+        _check(load_library().delta_set_nccl_library(path.encode()))
+    except ImportError:
+        pass
     buf = ctypes.create_string_buffer(128)
     _check(load_library().delta_nccl_get_unique_id(buf))
     return buf.raw

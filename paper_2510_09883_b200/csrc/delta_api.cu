@@ -252,18 +252,18 @@ struct NcclApi {
     ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
     const char* (*getErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
 };
+
+std::string g_nccl_path;  // delta_set_nccl_library (before the first NCCL use)
 
 const NcclApi& nccl() {
     static NcclApi api = [] {
         NcclApi a;
-        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);  // the copy already loaded, if any
+        if (!lib && !g_nccl_path.empty()) lib = dlopen(g_nccl_path.c_str(), RTLD_NOW | RTLD_GLOBAL);
         if (!lib) {
-            const char* env = std::getenv("DELTA_NCCL_LIB");
-            if (env) lib = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
-        }
-        if (!lib) {
-            a.why = "libnccl.so.2 not found (set DELTA_NCCL_LIB)";
+            a.why = "libnccl.so.2 not found (delta_set_nccl_library)";
             return a;
         }
         a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(lib, "ncclGetUniqueId"));
@@ -271,6 +271,7 @@ const NcclApi& nccl() {
         a.allGather = reinterpret_cast<decltype(a.allGather)>(dlsym(lib, "ncclAllGather"));
         a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(lib, "ncclCommDestroy"));
         a.getErrorString = reinterpret_cast<decltype(a.getErrorString)>(dlsym(lib, "ncclGetErrorString"));
+        a.commGetAsyncError = reinterpret_cast<decltype(a.commGetAsyncError)>(dlsym(lib, "ncclCommGetAsyncError"));
         a.ok = a.getUniqueId && a.commInitRank && a.allGather && a.commDestroy && a.getErrorString;
         if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
         return a;
@@ -1214,6 +1215,23 @@ delta_status delta_get_error(delta_t h, cudaStream_t stream, delta_status* stick
     if (e == cudaSuccess) e = cudaMemset(dev, 0, sizeof v);
     if (e != cudaSuccess) return cuda_fail(h, e, "get_error read");
     *sticky = (delta_status)v;
+    // sequence sharding with the library's communicator: surface asynchronous NCCL failures
+    // (a peer that died, a network error) — they would otherwise only show as a hang
+    if (h->comm && nccl().commGetAsyncError) {
+        ncclResult_t ar = ncclSuccess;
+        const ncclResult_t r = nccl().commGetAsyncError(h->comm, &ar);
+        if (r != ncclSuccess) return fail(h, DELTA_ERR_NCCL, std::string("ncclCommGetAsyncError: ") + nccl().getErrorString(r));
+        if (ar != ncclSuccess && ar != ncclInProgress) {
+            *sticky = DELTA_ERR_NCCL;
+            return fail(h, DELTA_ERR_NCCL, std::string("NCCL async error: ") + nccl().getErrorString(ar));
+        }
+    }
+    return DELTA_OK;
+}
+
+delta_status delta_set_nccl_library(const char* path) {
+    if (!path) return fail(nullptr, DELTA_ERR_USAGE, "null path");
+    g_nccl_path = path;
     return DELTA_OK;
 }
 
