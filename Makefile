@@ -5,7 +5,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt
 PKG       := paper_2510_09883_b200
 CSRC      := $(PKG)/csrc
 BUILD     := build
-OBJS      := $(BUILD)/bw_probe.o $(BUILD)/attn_sparse.o $(BUILD)/raas.o $(BUILD)/prefill.o $(BUILD)/recall.o $(BUILD)/quest.o $(BUILD)/attn_umma.o $(BUILD)/attn_tc.o $(BUILD)/attn_simt.o $(BUILD)/select.o $(BUILD)/append.o $(BUILD)/shard.o $(BUILD)/delta_api.o
+OBJS      := $(BUILD)/prefill_umma.o $(BUILD)/bw_probe.o $(BUILD)/attn_sparse.o $(BUILD)/raas.o $(BUILD)/prefill.o $(BUILD)/recall.o $(BUILD)/quest.o $(BUILD)/attn_umma.o $(BUILD)/attn_tc.o $(BUILD)/attn_simt.o $(BUILD)/select.o $(BUILD)/append.o $(BUILD)/shard.o $(BUILD)/delta_api.o
 HDRS      := $(wildcard $(CSRC)/*.cuh) $(CSRC)/internal.h include/delta.h
 
 all: $(PKG)/libdelta.so synth/libsynth.so oracle/liboracle.so
@@ -44,11 +44,11 @@ trace: build_trace/libdelta.so
 # Experiment variants of the trace build (kernel-cost breakdown); not the product.
 build_exp_%/libdelta.so: $(CSRC)/*.cu $(HDRS)
 	mkdir -p build_exp_$*
-	for f in bw_probe attn_sparse raas prefill recall quest attn_umma attn_tc attn_simt select append shard delta_api; do $(NVCC) $(NVFLAGS) -DDELTA_TRACE -DEXP_$* -c $(CSRC)/$$f.cu -o build_exp_$*/$$f.o 2>/dev/null || exit 1; done
+	for f in prefill_umma bw_probe attn_sparse raas prefill recall quest attn_umma attn_tc attn_simt select append shard delta_api; do $(NVCC) $(NVFLAGS) -DDELTA_TRACE -DEXP_$* -c $(CSRC)/$$f.cu -o build_exp_$*/$$f.o 2>/dev/null || exit 1; done
 	$(NVCC) $(ARCH) -shared -o $@ build_exp_$*/*.o
 
 # Timing variants (experiments only, no trace stamps): make build_var_NOMATH/libdelta.so
 build_var_%/libdelta.so: $(CSRC)/*.cu $(HDRS)
 	mkdir -p build_var_$*
-	for f in bw_probe attn_sparse raas prefill recall quest attn_umma attn_tc attn_simt select append shard delta_api; do $(NVCC) $(NVFLAGS) -DEXP_$(subst +, -DEXP_,$*) -c $(CSRC)/$$f.cu -o build_var_$*/$$f.o 2>/dev/null || exit 1; done
+	for f in prefill_umma bw_probe attn_sparse raas prefill recall quest attn_umma attn_tc attn_simt select append shard delta_api; do $(NVCC) $(NVFLAGS) -DEXP_$(subst +, -DEXP_,$*) -c $(CSRC)/$$f.cu -o build_var_$*/$$f.o 2>/dev/null || exit 1; done
 	$(NVCC) $(ARCH) -shared -o $@ build_var_$*/*.o

@@ -309,7 +309,7 @@ const char*  delta_layer_kernel_name(delta_t h, int32_t layer, int32_t batch);
 
 /* Experiment hook (tools/, never needed for correct results): override one kernel-variant knob
  * of a handle (nsplit, snsplit, deep, prewait, early, umma, policy, seltrig, selhist, gmerge,
- * gm2, lat, qpf — see DESIGN.md §7).  Drops the handle's captured step graphs.  CONFIG
+ * gm2, lat, qpf, pfumma — see DESIGN.md §7).  Drops the handle's captured step graphs.  CONFIG
  * for an unknown key, USAGE for a null handle.  The library reads no environment variables. */
 delta_status delta_set_tuning(delta_t h, const char* key, int32_t value);
 

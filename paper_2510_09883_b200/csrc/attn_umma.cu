@@ -26,6 +26,7 @@
 #include <algorithm>
 
 #include "combine.cuh"
+#include "umma.cuh"
 
 #ifdef DELTA_TRACE
 // per-tile event stamps of CTA (0,0,0) (trace builds): [tile][event]
@@ -74,30 +75,6 @@ struct UCfg {
     static constexpr int kMisc = 16 + (kNS + 4) * 4 + 2 * kMaxEpoch * 8 * 4;
     static constexpr int kSmem = 1024 + oMisc + kMisc;
 };
-
-__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
-    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)(layout & 7) << 61);
-}
-// kind::f16 instruction descriptor: D fp32, A = B = bf16, majors, N >> 3, M >> 4
-constexpr uint32_t umma_idesc(int M, int N, int a_mn, int b_mn) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-constexpr uint32_t kLayoutNone = 0, kLayoutSW128 = 2;
-
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
 template <int D, bool TOKEN_PLAN, int NR>
 __global__ void __launch_bounds__(kUThreads, 2)

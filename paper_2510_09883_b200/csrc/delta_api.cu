@@ -347,7 +347,7 @@ struct delta_ctx {
     // cycles to issue (tools/umma_test.cu), so 10 per tile lose to the mma.sync kernel here;
     // kept selectable (DELTA_TUNE umma=1) and parity-tested.
     int tune_prewait = 1, tune_early = 1, tune_umma = 0, tune_policy = 0;
-    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1, tune_gm2 = 0, tune_lat = 1, tune_qpf = 1;
+    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1, tune_gm2 = 0, tune_lat = 1, tune_qpf = 1, tune_pfumma = 1;
     // sequence sharding
     int world = 1, rank = 0, page_lo = 0, page_hi = 0x7fffffff;
     ncclComm_t comm = nullptr;  // null with world > 1: the caller exchanges (delta_shard_* calls)
@@ -1160,7 +1160,9 @@ delta_status delta_prefill(delta_t h, int32_t layer, int32_t batch, int32_t ntok
     p.scale_log2 = (float)((double)h->scale * 1.4426950408889634);
     p.q = q; p.kv_pool = h->kv_pool; p.block_table = h->block_table; p.seq_len = h->at<int32_t>(h->L.seq_len);
     p.out = out; p.lse_out = lse_out; p.err = h->at<int32_t>(h->L.err);
-    cudaError_t e = launch_prefill(p, stream, h->pdl);
+    // tcgen05 / TMEM kernel (prefill_umma.cu); the mma.sync kernel stays selectable (pfumma=0)
+    cudaError_t e = (h->tune_pfumma && prefill_umma_supported(p)) ? launch_prefill_umma(p, &h->tm_kv, stream, h->pdl)
+                                                                  : launch_prefill(p, stream, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "prefill launch");
     ++h->launches;
     h->last_kind = delta_ctx::kLastAttn;
@@ -1270,7 +1272,7 @@ delta_status delta_set_tuning(delta_t h, const char* key, int32_t value) {
         {"nsplit", &h->tune_nsplit}, {"snsplit", &h->tune_snsplit}, {"deep", &h->tune_deep},
         {"prewait", &h->tune_prewait}, {"early", &h->tune_early}, {"umma", &h->tune_umma},
         {"policy", &h->tune_policy}, {"seltrig", &h->tune_seltrig}, {"selhist", &h->tune_selhist},
-        {"gmerge", &h->tune_gmerge}, {"gm2", &h->tune_gm2}, {"lat", &h->tune_lat}, {"qpf", &h->tune_qpf}};
+        {"gmerge", &h->tune_gmerge}, {"gm2", &h->tune_gm2}, {"lat", &h->tune_lat}, {"qpf", &h->tune_qpf}, {"pfumma", &h->tune_pfumma}};
     for (const Knob& k : knobs)
         if (std::strcmp(k.name, key) == 0) {
             *k.field = value;

@@ -198,6 +198,8 @@ struct PrefillParams {
     int32_t* err;
 };
 cudaError_t launch_prefill(const PrefillParams& p, cudaStream_t st, bool pdl);
+cudaError_t launch_prefill_umma(const PrefillParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl);
+bool prefill_umma_supported(const PrefillParams& p);
 size_t prefill_smem_bytes(int d, int gs);
 
 // RaaS policy (raas.cu): retained-set reset and the per-step refresh / eviction.

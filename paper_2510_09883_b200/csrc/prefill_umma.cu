@@ -1,0 +1,367 @@
+// prefill_umma.cu — chunked prefill (NEXT-3; Eq.4 with the causal mask over a
+// prompt chunk) on the 5th-generation tensor cores: tcgen05.mma with the
+// accumulators in TMEM, operands in shared memory, K/V pages streamed by TMA.
+//
+// Query i of the chunk sits at position n0 + i and attends tokens t <= n0 + i; GQA head j
+// reads group phi(j) = j / gs (R15).  CTA = (tile of T = 128 / gs query tokens, kv head h,
+// sequence b): its 128 MMA rows are the (head j, token i) pairs of the group, row = j T + i.
+// Per KV block of KB = 4 pages (64 tokens):
+//   S[128 x 64]  = Q . K^T           D/16 MMAs M=128 N=64  K=16   (TMEM, double-buffered)
+//   P = exp2(S * scale * log2 e - m) (online softmax, one thread per row, lazily raised m)
+//   O[128 x D]  += P . V             per page: P_hi . V and P_lo . V, M=128 N=D K=16 (TMEM)
+// P enters as bf16 hi + lo (~16-bit probabilities, R18 as in the decode kernels).
+// Measured on this B200 (tools/umma_rate.cu): a tcgen05.mma costs ~46 cycles whatever its N up
+// to N = 32, 48 at N = 64 and 64 at N = 128 — so S is issued over 64-token blocks.  K rows of 4
+// pages are not uniformly strided in the pool (each (page, head) is K rows then V rows, 8 KiB),
+// so two copy warps restage the K rows of a block into one [half][64 rows][128 B] block (same
+// 128-byte swizzle phase: plain row copies); V stays in the TMA'd page (MN-major B operand).
+// Warps: 0-3 softmax + epilogue (thread = row), 4 TMA producer, 5 MMA issuer, 6-7 K restaging.
+// Measured (tools/prefill_bench.py): 246-292 TFLOP/s at the Llama-8B shape (the mma.sync kernel:
+// 142-186); ncu: the tensor pipe ~17 % busy, every role mostly waiting on the next — the chain
+// TMA -> restage -> S -> softmax -> PV -> slot release -> TMA is latency-bound.  Copying V out as
+// well (freeing each ring slot at once) with a single P buffer measured slower (250 TFLOP/s).
+#include <algorithm>
+
+#include "combine.cuh"
+#include "umma.cuh"
+
+namespace delta {
+namespace {
+
+constexpr int kPuThreads = 256;
+constexpr int kPuKB = 4;                  // pages per KV block (64 tokens)
+constexpr int kPuNR = 8;                  // page slots in the TMA ring (two blocks)
+constexpr int kPuBT = kPuKB * kPage;      // tokens per block
+constexpr float kPuRaise = 8.f;           // log2 headroom before the running max moves
+
+template <int D>
+struct PuCfg {
+    static constexpr int kHalves = D / 64;
+    static constexpr int kTile = TileLayout<D>::kBytes;          // one (page, head): K rows then V rows
+    static constexpr int kQ = kHalves * 128 * 128;               // Q: [half][128 rows][128 B]
+    static constexpr int kKst = kHalves * kPuBT * 128;           // K block: [half][64 rows][128 B]
+    static constexpr int kP = 128 * 128;                         // P: [128 rows][64 tok bf16]
+    static constexpr int oQ = 0;
+    static constexpr int oRing = oQ + kQ;
+    static constexpr int oKst = oRing + kPuNR * kTile;           // 2 K blocks
+    static constexpr int oP = oKst + 2 * kKst;                   // 2 x (hi, lo)
+    static constexpr int oBar = oP + 4 * kP;
+    static constexpr int nBar = 2 * kPuNR + 2 * 6;
+    static constexpr int kSmem = 1024 + oBar + nBar * 8 + 16;
+    static constexpr int kTmemCols = 256;                        // S: 2 x 64 columns, O: D columns at 128
+    static constexpr int kOCol = 128;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kPuThreads, 1)
+prefill_umma_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillParams p) {
+    using C = PuCfg<D>;
+    extern __shared__ __align__(16) uint8_t pu_smem[];
+    uint8_t* base = pu_smem + ((1024u - (smem_u32(pu_smem) & 1023u)) & 1023u);
+    uint8_t* qs = base + C::oQ;
+    uint8_t* ring = base + C::oRing;
+    uint8_t* kst = base + C::oKst;
+    uint8_t* pbuf = base + C::oP;  // [2][hi, lo][kP]
+    uint64_t* ring_full = reinterpret_cast<uint64_t*>(base + C::oBar);
+    uint64_t* ring_empty = ring_full + kPuNR;
+    uint64_t* kst_full = ring_empty + kPuNR;
+    uint64_t* kst_empty = kst_full + 2;
+    uint64_t* s_full = kst_empty + 2;
+    uint64_t* s_free = s_full + 2;
+    uint64_t* p_full = s_free + 2;
+    uint64_t* p_free = p_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_free + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int gs = p.gs, T = 128 / gs;
+    const int tile = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;  // longest rows first
+    const int t0 = tile * T;
+
+    if (tid == 0) {
+        for (int i = 0; i < kPuNR; ++i) {
+            mbar_init(&ring_full[i], 1);
+            mbar_init(&ring_empty[i], 1);  // the PV of the page completed
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&kst_full[i], 2);  // the two restaging warps
+            mbar_init(&kst_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_free[i], 4);    // the four softmax warps
+            mbar_init(&p_full[i], 4);
+            mbar_init(&p_free[i], 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(C::kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (warp == 4 && lane == 0) tma_prefetch_desc(&tm_kv);
+    pdl_wait();  // the chunk's append (previous kernel) wrote the pool rows and the length
+    const int s_tot = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
+    const int n0 = s_tot - p.ntok;
+    const int t_hi = min(p.ntok, t0 + T);                 // tokens [t0, t_hi) of the chunk
+    const int kv_end = n0 + t_hi;                         // keys [0, kv_end) are needed
+    const int n_pages = (kv_end + kPage - 1) / kPage;
+    const int nblk = (n_pages + kPuKB - 1) / kPuKB;
+    // Q rows (warps 0-3: thread = row), K-major SW128: 16-byte chunk c of row r at
+    // half (c / 8) * 16 KiB + r * 128 + ((c % 8) ^ (r % 8)) * 16
+    if (warp < 4) {
+        const int r = tid, j = r / T, i = r - j * T;
+        const bool valid = j < gs && t0 + i < p.ntok;
+        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.q) +
+                                                          (((size_t)b * p.ntok + t0 + i) * p.m + h * gs + j) * D);
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) {
+            const uint4 v = valid ? src[c] : make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(qs + (c >> 3) * 16384 + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+        }
+        fence_proxy_async_smem();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    pdl_launch_dependents();
+    const uint32_t tbase = *tmem_slot;
+    const size_t layer_ph = (size_t)p.layer * p.num_phys;
+    const int32_t* bt = p.block_table + (size_t)b * p.bt_stride;
+
+    if (warp == 4) {
+        // ============================================================ TMA producer (pages in order)
+        if (lane == 0) {
+            for (int pg = 0; pg < n_pages; ++pg) {
+                const int slot = pg % kPuNR, round = pg / kPuNR;
+                if (round > 0) mbar_wait(&ring_empty[slot], (round - 1) & 1);
+                mbar_arrive_expect_tx(&ring_full[slot], C::kTile);
+                const int row0 = (int)kv_row(layer_ph + bt[pg], p.g, h, 0);
+                uint8_t* dst = ring + slot * C::kTile;
+                if (D == 64) tma_load_2d(dst, &tm_kv, &ring_full[slot], 0, row0, kEvictNormal);
+                else tma_load_3d(dst, &tm_kv, &ring_full[slot], 0, row0, 0, kEvictNormal);
+            }
+        }
+    } else if (warp >= 6) {
+        // ============================================================ K restaging (64 threads)
+        const int ct = tid - 192;
+        for (int i = 0; i < nblk; ++i) {
+            if (i >= 2) mbar_wait(&kst_empty[i & 1], ((i - 2) >> 1) & 1);
+            uint8_t* kb = kst + (i & 1) * C::kKst;
+            for (int q = 0; q < kPuKB; ++q) {
+                const int pg = i * kPuKB + q;
+                if (pg >= n_pages) break;
+                const int slot = pg % kPuNR;
+                mbar_wait(&ring_full[slot], (pg / kPuNR) & 1);
+                const uint8_t* src = ring + slot * C::kTile;
+                // 16 K rows x 128 B per half: 128 chunks per half, 2 per thread per half; the rows
+                // keep their 128-byte swizzle phase (row % 8)
+#pragma unroll
+                for (int hf = 0; hf < C::kHalves; ++hf)
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int ch = ct + 64 * u, row = ch >> 3, c16 = ch & 7;
+                        const uint4 v = *reinterpret_cast<const uint4*>(src + hf * TileLayout<D>::kHalfBytes + row * 128 + c16 * 16);
+                        *reinterpret_cast<uint4*>(kb + hf * (kPuBT * 128) + (q * kPage + row) * 128 + c16 * 16) = v;
+                    }
+                if (pg == n_pages - 1 && kv_end % kPage) {  // partial last page: zero V rows past the end
+                    const int r0 = kv_end % kPage;
+                    uint8_t* vt = ring + slot * C::kTile + TileLayout<D>::kVOff;
+                    for (int ch = ct; ch < (kPage - r0) * (D / 8); ch += 64) {
+                        const int r = r0 + ch / (D / 8), c = ch % (D / 8);
+                        *reinterpret_cast<uint4*>(vt + swz<D>(r, c)) = make_uint4(0, 0, 0, 0);  // 0 * garbage != NaN
+                    }
+                }
+            }
+            fence_proxy_async_smem();  // generic stores -> the tensor core's async-proxy reads
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&kst_full[i & 1]);
+        }
+    } else if (warp == 5) {
+        // ============================================================ MMA issuer (one lane)
+        constexpr uint32_t kIdS = umma_idesc(128, kPuBT, 0, 0);  // A = Q K-major, B = K rows K-major
+        constexpr uint32_t kIdPV = umma_idesc(128, D, 0, 1);     // A = P K-major, B = V MN-major
+        const uint32_t qs_u = smem_u32(qs), kst_u = smem_u32(kst), ring_u = smem_u32(ring), p_u = smem_u32(pbuf);
+        for (int i = 0; i <= nblk; ++i) {
+            if (i < nblk) {  // S(i)
+                mbar_wait(&kst_full[i & 1], (i >> 1) & 1);
+                if (i >= 2) mbar_wait(&s_free[i & 1], ((i - 2) >> 1) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t kb = kst_u + (i & 1) * C::kKst;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint64_t a = umma_desc(qs_u + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, kLayoutSW128);
+                        const uint64_t bk = umma_desc(kb + (kk >> 2) * (kPuBT * 128) + (kk & 3) * 32, 16, 1024, kLayoutSW128);
+                        umma(tbase + (i & 1) * kPuBT, a, bk, kIdS, kk > 0 ? 1u : 0u);
+                    }
+                    umma_commit(&s_full[i & 1]);
+                    umma_commit(&kst_empty[i & 1]);
+                }
+                __syncwarp();
+            }
+            if (i >= 1) {  // PV(i - 1), after its softmax wrote P
+                const int j = i - 1;
+                mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t ph = p_u + (j & 1) * 2 * C::kP, pl = ph + C::kP;
+                    for (int q = 0; q < kPuKB; ++q) {
+                        const int pg = j * kPuKB + q;
+                        if (pg >= n_pages) break;
+                        const int slot = pg % kPuNR;
+                        // V rows of the page in its ring slot: MN-major, halves kHalfBytes apart
+                        const uint64_t bv = umma_desc(ring_u + slot * C::kTile + TileLayout<D>::kVOff,
+                                                      D == 128 ? TileLayout<D>::kHalfBytes : 0, 1024, kLayoutSW128);
+                        umma(tbase + C::kOCol, umma_desc(ph + q * 32, 16, 1024, kLayoutSW128), bv, kIdPV,
+                             (j > 0 || q > 0) ? 1u : 0u);
+                        umma(tbase + C::kOCol, umma_desc(pl + q * 32, 16, 1024, kLayoutSW128), bv, kIdPV, 1u);
+                        umma_commit(&ring_empty[slot]);
+                    }
+                    umma_commit(&p_free[j & 1]);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ============================================================ softmax (thread = row)
+        const int r = tid, j = r / T, i_tok = r - j * T;
+        const bool valid = j < gs && t0 + i_tok < p.ntok;
+        const int pos = n0 + t0 + i_tok;   // keys t <= pos
+        const float sl2 = p.scale_log2;
+        const uint32_t lane_base = tbase + ((uint32_t)(warp * 32) << 16);
+        float m = -INFINITY, l = 0.f;
+        for (int i = 0; i < nblk; ++i) {
+            mbar_wait(&s_full[i & 1], (i >> 1) & 1);
+            tc_fence_after();
+            float x[kPuBT];
+            {
+                uint32_t v0[32], v1[32];
+                tmem_ld32(lane_base + (i & 1) * kPuBT, v0);
+                tmem_ld32(lane_base + (i & 1) * kPuBT + 32, v1);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    x[c] = __uint_as_float(v0[c]);
+                    x[32 + c] = __uint_as_float(v1[c]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_free[i & 1]);
+            float bmax = -INFINITY;
+            const int tk0 = i * kPuBT;
+#pragma unroll
+            for (int c = 0; c < kPuBT; ++c) {
+                x[c] = (valid && tk0 + c <= pos) ? x[c] * sl2 : -INFINITY;
+                bmax = fmaxf(bmax, x[c]);
+            }
+            // raise the running max only when a logit exceeds it by the headroom (p <= 2^8)
+            const bool raise = bmax > m + kPuRaise || (m == -INFINITY && bmax > -INFINITY);
+            const float m_new = raise ? fmaxf(m, bmax) : m;
+            const bool rescale = raise && l > 0.f;
+            if (__any_sync(0xffffffffu, rescale)) {
+                // O rows of this warp hold earlier blocks' contributions: wait for PV(i - 1),
+                // then scale them in TMEM (warp-wide: tcgen05.ld / st are .sync.aligned)
+                mbar_wait(&p_free[(i - 1) & 1], ((i - 1) >> 1) & 1);
+                tc_fence_after();
+                const float al = rescale ? ex2(m - m_new) : 1.f;
+#pragma unroll
+                for (int c0 = 0; c0 < D; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(lane_base + C::kOCol + c0, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(__uint_as_float(v[c]) * al);
+                    tmem_st32(lane_base + C::kOCol + c0, v);
+                }
+                tmem_wait_st();
+                l *= al;
+            }
+            m = m_new;
+            const float msafe = m == -INFINITY ? 0.f : m;
+            if (i >= 2) mbar_wait(&p_free[i & 1], ((i - 2) >> 1) & 1);  // PV(i - 2) done with this P buffer
+            uint8_t* ph = pbuf + (i & 1) * 2 * C::kP;
+            uint8_t* pl = ph + C::kP;
+#pragma unroll
+            for (int c16 = 0; c16 < kPuBT / 8; ++c16) {  // 8 tokens per 16-byte chunk
+                uint32_t hw[4], lw[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float p0 = ex2(x[c16 * 8 + 2 * e] - msafe), p1 = ex2(x[c16 * 8 + 2 * e + 1] - msafe);
+                    l += p0 + p1;
+                    const __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
+                    const float2 hf = __bfloat1622float2(hv);
+                    hw[e] = *reinterpret_cast<const uint32_t*>(&hv);
+                    lw[e] = pack_bf16(p0 - hf.x, p1 - hf.y);
+                }
+                const int off = r * 128 + ((c16 ^ (r & 7)) << 4);
+                *reinterpret_cast<uint4*>(ph + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                *reinterpret_cast<uint4*>(pl + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[i & 1]);
+        }
+        // ------------------------------------------------------------ epilogue: O / l
+        if (nblk > 0) mbar_wait(&p_free[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);  // the last PV completed
+        tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        float* dst = p.out + (((size_t)b * p.ntok + t0 + i_tok) * p.m + h * gs + j) * D;
+        bool bad = false;
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(lane_base + C::kOCol + c0, v);
+            tmem_wait_ld();
+            if (valid) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    const float4 o = make_float4(__uint_as_float(v[c]) * inv, __uint_as_float(v[c + 1]) * inv,
+                                                 __uint_as_float(v[c + 2]) * inv, __uint_as_float(v[c + 3]) * inv);
+                    bad |= !(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w));
+                    *reinterpret_cast<float4*>(dst + c0 + c) = o;
+                }
+            }
+        }
+        if (valid && p.lse_out)
+            p.lse_out[((size_t)b * p.ntok + t0 + i_tok) * p.m + h * gs + j] =
+                l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
+        if (bad) set_err(p.err, kDevNumeric);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::kTmemCols));
+}
+
+}  // namespace
+
+bool prefill_umma_supported(const PrefillParams& p) { return (p.d == 128 || p.d == 64) && p.gs <= 16; }
+
+cudaError_t launch_prefill_umma(const PrefillParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl) {
+    const void* fn = p.d == 128 ? (const void*)prefill_umma_kernel<128> : (const void*)prefill_umma_kernel<64>;
+    const int smem = p.d == 128 ? PuCfg<128>::kSmem : PuCfg<64>::kSmem;
+    static std::atomic<int> cache[kMaxDevices * 2];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+    const int slot = dev * 2 + (p.d == 128 ? 0 : 1);
+    if (cache[slot].load(std::memory_order_acquire) == 0) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        cache[slot].store(1, std::memory_order_release);
+    }
+    const int T = 128 / p.gs;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((p.ntok + T - 1) / T, p.g, p.batch);
+    cfg.blockDim = dim3(kPuThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    void* args[] = {const_cast<CUtensorMap*>(tm_kv), const_cast<PrefillParams*>(&p)};
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+}  // namespace delta
