@@ -603,14 +603,17 @@ def run_ours(args, c):
                            n_sparse_l * us_sparse_graph / us_step)
     else:
         roof_sparse = roof("SPARSE layer kernel, one layer (eager)", sp_bytes, us_sparse, "eager back-to-back", None)
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_full_decode_traffic.json")
-    if os.path.exists(prof):
+    # DRAM traffic per launch from one ncu --set full capture of the same kernels at C1
+    # (profiles/r2/ncu_traffic.json); other configs: not captured (null)
+    roof_full["traffic"] = roof_sparse["traffic"] = None
+    prof = os.path.join(ROOT, "profiles", "r2", "ncu_traffic.json")
+    if os.path.exists(prof) and args.config == "c1":
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            tr = json.load(open(prof))
+            roof_full["traffic"] = tr.get("full", {}).get("dram_bytes_per_launch")
+            roof_sparse["traffic"] = tr.get("sparse", {}).get("dram_bytes_per_launch")
         except Exception:
-            traffic = None
-    roof_full["traffic"] = traffic
+            pass
     # "roofline" = the kernel with the largest share of the DELTA step's time
     dominant = roof_full if (roof_sparse["share_of_step"] or 0) <= roof_full["share_of_step"] else roof_sparse
     kernels = {

@@ -42,7 +42,7 @@ def smid_report(layer, ncta, tr=None):
     per = np.bincount(ids, minlength=148)
     print(f"   placement L{layer}: {int((per > 0).sum())} SMs used, {int((per == 2).sum())} with 2 CTAs, "
           f"{int((per > 2).sum())} with >2")
-    if tr is not None:  # loop-done time of CTAs alone on their SM vs sharing it
+    if tr is not None and (tr[layer, :ncta, 0] > 0).any():  # loop-done time alone vs sharing the SM
         t = tr[layer, :ncta].astype(np.int64)
         t0 = t[:, 0][t[:, 0] > 0].min()
         ld = (t[:, 3] - t0) / 1e3
