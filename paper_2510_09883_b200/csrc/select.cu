@@ -16,6 +16,27 @@
 #define DTRACE_LAYER_OFF 32  // trace builds: select stamps go to layer slot + 32
 #include "combine.cuh"
 
+#ifdef DELTA_TRACE
+// per-warp SM-clock stamps of phase A (trace builds): [layer][cta][warp][8]
+static __device__ long long g_sel_clk[64 * 160 * 16 * 8];
+extern "C" int delta_trace_read_select_clk(void* host, size_t bytes) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess)
+        e = cudaMemcpyFromSymbol(host, g_sel_clk, bytes < sizeof(g_sel_clk) ? bytes : sizeof(g_sel_clk));
+    void* dev = nullptr;
+    if (e == cudaSuccess) e = cudaGetSymbolAddress(&dev, g_sel_clk);
+    if (e == cudaSuccess) e = cudaMemset(dev, 0, sizeof(g_sel_clk));
+    return (int)e;
+}
+#define SELCLK(ev)                                                                                       \
+    do {                                                                                                 \
+        if ((threadIdx.x & 31) == 0 && blockIdx.x < 160 && p.layer < 64 && blockIdx.y == 0)              \
+            g_sel_clk[((p.layer * 160 + blockIdx.x) * 16 + (threadIdx.x >> 5)) * 8 + (ev)] = clock64(); \
+    } while (0)
+#else
+#define SELCLK(ev) do {} while (0)
+#endif
+
 namespace delta {
 namespace {
 
@@ -301,7 +322,16 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
     if (!p.late_trigger) pdl_launch_dependents();  // the next kernel's reads of this plan come after its own wait
     if (tid == 0) DTRACE(1);
 
-    int s = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
+    SELCLK(0);
+    // Per-CTA broadcast of the values every warp needs (length counter, the LSE row): every
+    // warp of every CTA loading the same words makes an L2 hot spot (measured: ~1850 cycles for
+    // the length load, ~2800 for the LSE + logits, against ~300 for an uncontended L2 hit)
+    __shared__ int s_len;
+    __shared__ __align__(16) float s_lse[256];
+    if (tid == 0) s_len = p.seq_len[p.layer * p.max_batch + b];
+    if (!p.keys_override && !p.k_new && tid < p.m) s_lse[tid] = p.lse_buf[(size_t)b * p.m + tid];
+    __syncthreads();
+    int s = s_len / p.g;  // raw counter = n * g
     if (p.k_new) {
         // Quest layer: Eq.7 append of this step's token at position s, then
         // fold it into its page's min/max representatives (quest.cu); a token in slot 0 starts
@@ -348,7 +378,7 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
 
     // ------------------------------------------------------------ phase A: scores
     if (!p.keys_override) {
-        const float* lse_g = p.lse_buf + (size_t)b * p.m;
+        const float* lse_g = s_lse;  // broadcast above (m <= 256)
         LseLane lsl;
         {
             const int hh0 = lane & 1, n4 = p.m >> 2;
@@ -361,6 +391,10 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
         }
         const int per = (n_units + p.nchunk - 1) / p.nchunk;
         const int u_lo = blockIdx.x * per, u_hi = min(n_units, u_lo + per);
+#ifdef DELTA_TRACE
+        if (u_hi == -12345) lsl.v[0].x += 1.f;  // orders the stamp after the length load
+#endif
+        SELCLK(1);
         const float* lg = p.logits + (size_t)b * p.max_seq * p.m;
         const int jr = lane >> 1, hh = lane & 1;
         // a warp handles 16 consecutive tokens: lane = 2*token + half-of-heads
@@ -375,11 +409,13 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
                 float mx = -INFINITY;
                 if (t < s && own) mx = head_max(lg + (size_t)t * p.m, lsl, lse_g, p.m, hh);
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+                if (u == u_lo + warp) SELCLK(2);
                 const float e = (t < s) ? expf(mx) : 0.f;
                 float sum = 0.f;
 #pragma unroll
                 for (int r = 0; r < kPage; ++r) sum += __shfl_sync(0xffffffffu, e, 2 * r);  // ascending t
                 if (lane == 0) keys_b[u] = (u * kPage >= own_lo && u * kPage < own_hi) ? sum : -INFINITY;
+                if (u == u_lo + warp) SELCLK(3);
             }
         } else {
             const int t_lo = u_lo, t_hi = u_hi;  // block == 1: units are tokens
@@ -395,6 +431,7 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
         // arrival: the barrier puts every thread's key stores before thread 0's acq_rel atomic
         // (release, cumulative); the last arrival's acquire + the barrier order its threads'
         // key loads after every other CTA's stores — no per-thread fences
+        SELCLK(4);
         __syncthreads();
         if (tid == 0) DTRACE(2);
         if (tid == 0) {
@@ -403,6 +440,10 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
             s_flag = (old == p.nchunk - 1);
         }
         __syncthreads();
+#ifdef DELTA_TRACE
+        if (s_flag == 7) s = 0;  // orders the stamp after the election
+#endif
+        SELCLK(5);
         if (!s_flag) return;
         if (tid == 0) DTRACE(3);
         if (tid == 0) p.cnt[b] = 0;

@@ -114,7 +114,7 @@ __global__ void gt_lat(int reps, int slot) {
 }
 
 int main() {
-    const int n_l2 = 1 << 20;          // 4 MB ring: L2 resident
+    const int n_l2 = 1 << 16;          // 256 KB ring, fully warmed: L2 resident
     const int n_hbm = 1 << 28;         // 1 GB ring: misses
     int *ring_l2, *ring_hbm;
     int idx_start = 0;
@@ -122,7 +122,7 @@ int main() {
     CK(cudaMalloc(&ring_hbm, (size_t)n_hbm * 4));
     {   // random permutation cycles with a large stride (defeat prefetch)
         std::vector<int> h(n_l2);
-        for (int i = 0; i < n_l2; ++i) h[i] = (int)(((long long)i * 4099 + 12345) % n_l2) & ~31;
+        for (int i = 0; i < n_l2; ++i) h[i] = (i + 32 * 37) % n_l2;  // stride 37 lines: one 4096-hop cycle
         CK(cudaMemcpy(ring_l2, h.data(), (size_t)n_l2 * 4, cudaMemcpyHostToDevice));
         std::vector<int> g(n_hbm / 1024);
         // sparse chain in the big ring: element k*1024*stride hops
@@ -134,7 +134,7 @@ int main() {
         idx_start = idx[0];
     }
     long long out[64];
-    chase<<<1, 32>>>(ring_l2, 4096, 2000, 0);
+    chase<<<1, 32>>>(ring_l2, 8192, 2000, 0);
     chase_cold<<<1, 32>>>(ring_hbm, idx_start, 2000, 1);
     bar_lat<<<1, 256>>>(1000, 2);
     bar_lat<<<1, 1024>>>(1000, 3);
@@ -150,7 +150,7 @@ int main() {
     gt_lat<<<1, 32>>>(1000, 13);
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpyFromSymbol(out, g_out, sizeof out));
-    const char* names[] = {"L2-hit dependent load", "HBM dependent load (TLB mostly hit)", "__syncthreads 256 thr",
+    const char* names[] = {"L2-hit dependent load (warmed 256 KB ring)", "HBM dependent load (TLB mostly hit)", "__syncthreads 256 thr",
                            "__syncthreads 1024 thr", "smem atomicAdd spread, 1024 thr (per round)",
                            "smem atomicAdd same addr, 1024 thr (per round)", "__match_any_sync", "shfl_xor + fadd",
                            "mma.sync m16n8k16 bf16, 1 chain (per mma)", "mma.sync 4 chains, 1 warp (per round of 4)",
