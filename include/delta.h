@@ -106,6 +106,15 @@ typedef struct {
                                   (delta_shard_exchange_buffers) and calls delta_shard_merge /
                                   delta_shard_select_merge (used for single-GPU simulation). */
     int32_t policy;            /* delta_policy (0 = DELTA) */
+    int32_t det_chunks;        /* C: 0 = off.  R21 run-to-run AND cross-W determinism: the pages
+                                  [0, ceil(max_seq_len/P)) are cut into C fixed chunks of
+                                  ceil(pages/C) pages; every layer attends each chunk separately
+                                  (same kernel and split count whatever W is) and LSE-merges the
+                                  C chunk partials in chunk order, Delta plans are ranged per
+                                  chunk — so outputs, LSEs and plans are bitwise identical for
+                                  every W dividing C (rank r holds chunks [r C/W, (r+1) C/W)).
+                                  Costs C/W attention launches + 1 merge per layer.  DELTA
+                                  policy only; C % W == 0, C <= 64. */
 } delta_config;
 
 /* Caller-owned device buffers.  Sizes from delta_query_sizes. */

@@ -38,7 +38,7 @@ class _Config(ctypes.Structure):
         ("budget_k", ctypes.c_int32), ("n_sink", ctypes.c_int32), ("n_window", ctypes.c_int32),
         ("select_block", ctypes.c_int32), ("kv_dtype", ctypes.c_int), ("softmax_scale", ctypes.c_float),
         ("shard_world", ctypes.c_int32), ("shard_rank", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
-        ("policy", ctypes.c_int32),
+        ("policy", ctypes.c_int32), ("det_chunks", ctypes.c_int32),
     ]
 
 
@@ -162,6 +162,7 @@ class DeltaConfig:
     shard_rank: int = 0
     nccl_id: bytes | None = None   # 128 bytes from nccl_unique_id() (rank 0), or None
     policy: int = POLICY_DELTA
+    det_chunks: int = 0            # R21 fixed chunks (bitwise identical results for every W | C)
 
     def to_c(self):
         arr = (ctypes.c_int32 * max(1, len(self.select_layers)))(*self.select_layers)
@@ -170,7 +171,8 @@ class DeltaConfig:
                     self.max_seq_len, self.page_size, self.num_phys_pages, self.num_full_prefix,
                     len(self.select_layers), arr, self.budget_k, self.n_sink, self.n_window, self.select_block,
                     self.kv_dtype, self.softmax_scale, self.shard_world, self.shard_rank,
-                    ctypes.cast(nid, ctypes.c_void_p) if nid is not None else None, self.policy)
+                    ctypes.cast(nid, ctypes.c_void_p) if nid is not None else None, self.policy,
+                    self.det_chunks)
         return c, (arr, nid)  # keep alive
 
     @property

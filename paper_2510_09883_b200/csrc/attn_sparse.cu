@@ -219,7 +219,7 @@ __device__ __forceinline__ void sp_epilogue(const AttnParams& p, const float* ms
     float* sM = stage + ClusterStage<D>::kO4 * 4;  // float2 (M_c, L_c) per [rank][row]
     uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage) + ClusterStage<D>::kBarOff);
     const uint32_t sO_u = smem_u32(sO), sM_u = smem_u32(sM), bar_u = smem_u32(bar);
-    const bool shard = p.shard_world > 1;
+    const bool shard = p.part_o != nullptr;
     bool bad = false;
     auto emit = [&](int row, int c4, float M, float L, float4 v) {
         const float inv = (L > 0.f) ? __frcp_rn(L) : 0.f;

@@ -199,7 +199,7 @@ __device__ __forceinline__ void cluster_epilogue(const AttnParams& p, const floa
                 bad1 = true;
             }
             const int j = h * gs + row;
-            const bool shard = p.shard_world > 1;
+            const bool shard = p.part_o != nullptr;
             reinterpret_cast<float4*>((shard ? p.part_o : p.out) + ((size_t)b * p.m + j) * D)[c4] = o;
             if (c4 == 0) {
                 const float lse = (L > 0.f) ? (M + log2f(L)) * kLn2 : -INFINITY;
@@ -292,7 +292,7 @@ __device__ __forceinline__ void cluster_epilogue(const AttnParams& p, const floa
                     bad = true;
                 }
                 const int j = h * gs + row;
-                const bool shard = p.shard_world > 1;  // the rank's partial; shard.cu merges the ranks
+                const bool shard = p.part_o != nullptr;  // the rank's partial; shard.cu merges the ranks
                 reinterpret_cast<float4*>((shard ? p.part_o : p.out) + ((size_t)b * p.m + j) * D)[c4] = o;
                 if (c4 == 0) {
                     const float lse = (L > 0.f) ? (M + log2f(L)) * kLn2 : -INFINITY;
@@ -362,7 +362,7 @@ __device__ __forceinline__ void global_epilogue(const AttnParams& p, const float
     const int total = gs * C4;
     const size_t rec = (size_t)gpart_floats(D);
     float* my = p.gpart + (((size_t)b * p.g + h) * ns + split) * rec;
-    const bool shard = p.shard_world > 1;
+    const bool shard = p.part_o != nullptr;
     bool bad = false;
     auto emit = [&](int row, int c4, float M, float L, float4 v) {
         const float inv = (L > 0.f) ? __frcp_rn(L) : 0.f;

@@ -55,7 +55,9 @@ struct Layout {
         raas_last,
         reps_bytes, total;
     int gslots;  // split partial slots of the global-merge kernels
-    size_t shard_block, cand_block;  // bytes of one rank's attention partial / candidate block
+    size_t shard_block, cand_block;  // bytes of one rank's attention partial(s) / candidate block
+    size_t part_bytes;               // one attention partial (o [batch][m][d], lse [batch][m])
+    int det_chunks, chunk_pages;     // R21 fixed chunks (0 = off) and pages per chunk
     int max_units, plan_cap, n_delta, max_pages;
 };
 
@@ -129,6 +131,9 @@ std::string validate(const delta_config& c, std::vector<int>& role, std::vector<
         return "page-level selection needs budget_k % page_size == 0 (R6)";
     if (c.shard_world < 1 || c.shard_world > 64 || c.shard_rank < 0 || c.shard_rank >= c.shard_world)
         return "shard_world must be in [1, 64] and 0 <= shard_rank < shard_world";
+    if (c.det_chunks < 0 || c.det_chunks > 64 || (c.det_chunks > 0 && c.det_chunks % std::max(1, c.shard_world) != 0))
+        return "det_chunks must be 0 or a multiple of shard_world in [1, 64]";
+    if (c.det_chunks > 0 && c.policy != DELTA_POLICY_DELTA) return "det_chunks needs the DELTA policy";
     if (c.softmax_scale < 0.f || !std::isfinite(c.softmax_scale)) return "softmax_scale must be finite and >= 0";
     if (c.policy != DELTA_POLICY_DELTA && c.policy != DELTA_POLICY_QUEST && c.policy != DELTA_POLICY_RAAS)
         return "policy must be DELTA, QUEST or RAAS";
@@ -208,14 +213,20 @@ Layout layout(const delta_config& c, int sms) {
     L.plan_phys = take((size_t)nd * c.max_batch * L.plan_cap * 4);
     L.plan_count = take((size_t)nd * c.max_batch * 4);
     L.plan_stamp = take((size_t)nd * c.max_batch * 4);
-    L.plan_lo = take((size_t)nd * c.max_batch * 4);
-    L.plan_hi = take((size_t)nd * c.max_batch * 4);
-    {   // sequence sharding exchange buffers: partial (o [B][m][d], lse [B][m]) and candidates
+    L.det_chunks = c.det_chunks;
+    L.chunk_pages = c.det_chunks > 0 ? (L.max_pages + c.det_chunks - 1) / c.det_chunks : 0;
+    const int nranges = std::max(1, c.det_chunks);  // plan ranges per slot: one per chunk
+    L.plan_lo = take((size_t)nd * nranges * c.max_batch * 4);
+    L.plan_hi = take((size_t)nd * nranges * c.max_batch * 4);
+    {   // sequence sharding exchange buffers: partials (o [B][m][d], lse [B][m]) and candidates;
+        // with R21 chunks a rank sends its det_chunks / W chunk partials
         const int W = std::max(1, c.shard_world);
-        L.shard_block = W > 1 ? align_up((size_t)c.max_batch * m * (D + 1) * 4) : 0;
+        const bool parts = W > 1 || c.det_chunks > 0;
+        L.part_bytes = parts ? align_up((size_t)c.max_batch * m * (D + 1) * 4) : 0;
+        L.shard_block = L.part_bytes * (c.det_chunks > 0 ? c.det_chunks / W : 1);
         L.cand_block = W > 1 && has_sel ? align_up((size_t)c.max_batch * L.plan_cap * 8) : 0;
         L.shard_send = take(L.shard_block);
-        L.shard_recv = take(L.shard_block * W);
+        L.shard_recv = take(W > 1 ? L.shard_block * W : 0);
         L.cand_send = take(L.cand_block);
         L.cand_recv = take(L.cand_block * W);
     }
@@ -280,10 +291,12 @@ const NcclApi& nccl() {
 }
 
 // Static page range of a rank: contiguous, page-aligned shares of the max_seq_len pages.
+// With R21 chunks a rank's range is the union of its det_chunks / W consecutive chunks.
 void shard_pages(const delta_config& c, int rank, int* lo, int* hi) {
     const int max_pages = (c.max_seq_len + kPage - 1) / kPage;
     const int W = std::max(1, c.shard_world);
-    const int per = (max_pages + W - 1) / W;
+    const int per = c.det_chunks > 0 ? (max_pages + c.det_chunks - 1) / c.det_chunks * (c.det_chunks / W)
+                                      : (max_pages + W - 1) / W;
     *lo = std::min(max_pages, rank * per);
     *hi = std::min(max_pages, (rank + 1) * per);
     if (W == 1) { *lo = 0; *hi = 0x7fffffff; }
@@ -409,16 +422,16 @@ AttnParams attn_params(delta_ctx* h, int layer, int batch, int role_override = -
     } else {
         p.nsplit = nsplit_full(batch, c.num_kv_heads, h->sms, h->L.max_pages);
     }
-    p.shard_world = h->world;
     p.page_lo = h->page_lo;
     p.page_hi = h->page_hi;
-    if (h->world > 1) {
+    if (h->world > 1 || h->L.det_chunks) {  // partials for the merge (launch_decode sets each chunk's)
         p.part_o = h->at<float>(h->L.shard_send);
         p.part_lse = p.part_o + (size_t)batch * c.num_q_heads * c.head_dim;
         if (p.role == kRoleSparse) {
             const int sl = h->slot[h->gov[layer]];
-            p.plan_lo = h->at<int32_t>(h->L.plan_lo) + (size_t)sl * c.max_batch;
-            p.plan_hi = h->at<int32_t>(h->L.plan_hi) + (size_t)sl * c.max_batch;
+            const size_t nr = std::max(1, h->L.det_chunks);
+            p.plan_lo = h->at<int32_t>(h->L.plan_lo) + (size_t)sl * nr * c.max_batch;
+            p.plan_hi = h->at<int32_t>(h->L.plan_hi) + (size_t)sl * nr * c.max_batch;
         }
     }
     // (the tcgen05 and fp32 kernels keep the cluster merge)
@@ -438,7 +451,7 @@ AttnParams attn_params(delta_ctx* h, int layer, int batch, int role_override = -
     // SPARSE page plans at small batch: the latency kernel (attn_sparse.cu) when every split's
     // share of the plan fits its resident tiles and two layers' CTAs fit one wave
     if (p.role == kRoleSparse && !p.emit_logits && h->use_tc && !h->tune_umma && h->tune_lat &&
-        c.select_block == kPage && h->world == 1 && h->gs <= 8) {
+        c.select_block == kPage && h->world == 1 && !h->L.det_chunks && h->gs <= 8) {
         const int lim = sparse_lat_max_split(c.head_dim);
         int ns = h->tune_snsplit > 0 ? h->tune_snsplit : 12;
         ns = std::min(ns, lim);
@@ -485,10 +498,13 @@ delta_status shard_allgather(delta_ctx* h, size_t send_off, size_t recv_off, siz
 delta_status launch_merge(delta_ctx* h, int layer, int batch, float* out, float* lse_out, cudaStream_t st) {
     const delta_config& c = h->cfg;
     ShardMergeParams mp = {};
-    mp.world = h->world; mp.batch = batch; mp.m = c.num_q_heads; mp.d = c.head_dim; mp.role = h->role[layer];
-    mp.recv_o = h->at<float>(h->L.shard_recv);
+    // R21 chunks: the det_chunks partials in chunk order (one rank: its own send block), merged
+    // by the same fixed left fold whatever W is -> bitwise identical across W
+    mp.world = h->L.det_chunks ? h->L.det_chunks : h->world;
+    mp.batch = batch; mp.m = c.num_q_heads; mp.d = c.head_dim; mp.role = h->role[layer];
+    mp.recv_o = h->at<float>(h->world > 1 ? h->L.shard_recv : h->L.shard_send);
     mp.recv_lse = mp.recv_o + (size_t)batch * c.num_q_heads * c.head_dim;
-    mp.o_stride = mp.lse_stride = h->L.shard_block / 4;
+    mp.o_stride = mp.lse_stride = h->L.part_bytes / 4;
     mp.out = out; mp.lse_out = lse_out; mp.lse_buf = h->at<float>(h->L.lse_buf);
     mp.err = h->at<int32_t>(h->L.err);
     cudaError_t e = launch_shard_merge(mp, st, h->pdl);
@@ -596,12 +612,43 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
         p.prewait = 0;
     // bf16: the tcgen05/TMEM kernel for GQA groups of <= 8 heads, the mma.sync kernel otherwise;
     // fp32 caches: the CUDA-core kernel (no tensor-core rounding of fp32 inputs).
-    cudaError_t e = !h->use_tc ? launch_attn_simt(p, h->cfg.kv_dtype == DELTA_BF16, st, h->pdl)
-                    : p.sparse_lat ? launch_attn_sparse_lat(p, &h->tm_kv, st, h->pdl)
-                    : (h->tune_umma && umma_supported(p)) ? launch_attn_umma(p, &h->tm_kv, st, h->pdl)
-                                                          : launch_attn_tc(p, &h->tm_kv, st, h->pdl);
+    auto launch_attn = [&](const AttnParams& ap) {
+        return !h->use_tc ? launch_attn_simt(ap, h->cfg.kv_dtype == DELTA_BF16, st, h->pdl)
+               : ap.sparse_lat ? launch_attn_sparse_lat(ap, &h->tm_kv, st, h->pdl)
+               : (h->tune_umma && umma_supported(ap)) ? launch_attn_umma(ap, &h->tm_kv, st, h->pdl)
+                                                      : launch_attn_tc(ap, &h->tm_kv, st, h->pdl);
+    };
+    cudaError_t e = cudaSuccess;
+    if (h->L.det_chunks) {
+        // R21 fixed chunks: the token is appended first (the rank's pages), then one launch per
+        // chunk this rank holds, each over exactly that chunk's pages (or its plan entries) with
+        // the W-independent split count, into the chunk's slot of the send block
+        if (k_new) {
+            delta_status s = launch_append_impl(h, layer, batch, 1, k_new, v_new, st);
+            if (s != DELTA_OK) return s;
+        }
+        p.fuse_append = 0; p.k_new = p.v_new = nullptr;
+        p.prewait = 0;
+        const int per_rank = h->L.det_chunks / h->world;
+        const size_t mb = h->cfg.max_batch;
+        const int32_t* lo0 = p.plan_lo;
+        const int32_t* hi0 = p.plan_hi;
+        for (int i = 0; i < per_rank && e == cudaSuccess; ++i) {
+            const int chunk = h->rank * per_rank + i;
+            AttnParams cp = p;
+            cp.page_lo = chunk * h->L.chunk_pages;
+            cp.page_hi = cp.page_lo + h->L.chunk_pages;
+            cp.part_o = h->at<float>(h->L.shard_send + (size_t)i * h->L.part_bytes);
+            cp.part_lse = cp.part_o + (size_t)batch * h->cfg.num_q_heads * h->cfg.head_dim;
+            if (lo0) { cp.plan_lo = lo0 + chunk * mb; cp.plan_hi = hi0 + chunk * mb; }
+            e = launch_attn(cp);
+            if (e == cudaSuccess) ++h->launches;
+        }
+    } else {
+        e = launch_attn(p);
+        if (e == cudaSuccess) ++h->launches;
+    }
     if (e != cudaSuccess) return cuda_fail(h, e, "decode launch");
-    ++h->launches;
     h->last_kind = delta_ctx::kLastAttn;
     h->last_layer = layer;
     if (h->role[layer] == kRoleRaas) {  // refresh + evict -> the retained set of the next step
@@ -614,6 +661,7 @@ delta_status launch_decode(delta_ctx* h, int layer, int batch, const void* k_new
         if (s2 != DELTA_OK) return s2;
         return launch_merge(h, layer, batch, out, lse_out, st);
     }
+    if (h->world == 1 && h->L.det_chunks) return launch_merge(h, layer, batch, out, lse_out, st);
     return DELTA_OK;
 }
 
@@ -645,8 +693,16 @@ delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_ov
     p.shard_mode = shard_mode;
     p.page_lo = h->page_lo; p.page_hi = h->page_hi;
     p.cand_out = h->at<uint2>(h->L.cand_send);
-    p.plan_lo = h->at<int32_t>(h->L.plan_lo) + (size_t)sl * c.max_batch;
-    p.plan_hi = h->at<int32_t>(h->L.plan_hi) + (size_t)sl * c.max_batch;
+    {   // plan ranges for the sharded attention: each R21 chunk, else this rank's pages
+        const size_t nr = std::max(1, h->L.det_chunks);
+        p.plan_lo = h->at<int32_t>(h->L.plan_lo) + (size_t)sl * nr * c.max_batch;
+        p.plan_hi = h->at<int32_t>(h->L.plan_hi) + (size_t)sl * nr * c.max_batch;
+        if (h->L.det_chunks && shard_mode != 1) {
+            p.range_n = h->L.det_chunks; p.range_first = 0; p.range_step = h->L.chunk_pages;
+        } else if (shard_mode == 2) {
+            p.range_n = 1; p.range_first = h->page_lo; p.range_step = h->page_hi - h->page_lo;
+        }
+    }
     p.err = h->at<int32_t>(h->L.err);
     cudaError_t e = launch_select(p, st, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "select launch");

@@ -85,13 +85,13 @@ struct AttnParams {
     const int32_t* plan_count;  // [max_batch]
     const int32_t* plan_stamp;  // [max_batch]
     int32_t* err;
-    // sequence sharding (shard_world > 1): this rank holds pages [page_lo, page_hi) of every
-    // sequence; attention covers only those, and the epilogue writes the rank's partial
-    // (normalised o, natural-log lse) instead of the outputs, for the cross-rank LSE merge.
-    int shard_world, page_lo, page_hi;
-    const int32_t* plan_lo;     // SPARSE, sharded: [max_batch] this rank's plan entries [lo, hi)
+    // sequence sharding / fixed chunks (R21): attention covers pages [page_lo, page_hi) of
+    // every sequence, and with part_o set the epilogue writes that range's partial (normalised
+    // o, natural-log lse) instead of the outputs, for the LSE merge (shard.cu).
+    int page_lo, page_hi;
+    const int32_t* plan_lo;     // SPARSE, sharded: [max_batch] the range's plan entries [lo, hi)
     const int32_t* plan_hi;
-    float* part_o;              // [batch][m][d]
+    float* part_o;              // [batch][m][d], or null: write out / lse_out
     float* part_lse;            // [batch][m]
 };
 
@@ -117,8 +117,11 @@ struct SelectParams {
     int32_t* err;
     // sequence sharding: mode 0 = unsharded; 1 = local (keys of own units only; export the
     // rank's top-k candidates to cand_out); 2 = global merge (keys_override = the dense keys
-    // scattered from all ranks' candidates; also writes this rank's plan range lo/hi)
+    // scattered from all ranks' candidates)
     int shard_mode, page_lo, page_hi;
+    // plan ranges (modes 2, and 0 with fixed chunks): for c < range_n, the plan entries on pages
+    // [range_first + c * range_step, + range_step) -> plan_lo/plan_hi[c * max_batch + b]
+    int range_n, range_first, range_step;
     uint2* cand_out;            // mode 1: [batch][k_units] (order-preserving key bits, unit)
     int late_trigger;           // 1: launch dependents after the plan is written (else at entry)
     // Quest layers: this launch also performs the layer's Eq.7 append of one token (pool rows,
@@ -129,7 +132,7 @@ struct SelectParams {
     void* reps;                 // [L][num_phys][g][2][d]
     int d, num_phys;
     int hist_mode;              // radix histogram: 0 per-warp private, 1 warp-aggregated shared
-    int32_t* plan_lo;           // [max_batch]
+    int32_t* plan_lo;           // [range_n][max_batch]
     int32_t* plan_hi;
 };
 

@@ -675,22 +675,26 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
         }
         return;  // the global plan comes from the merge pass (shard_mode 2)
     }
-    if (p.shard_mode == 2 && tid < 32) {
-        // this rank's sub-range of the ascending global plan: units on its pages
-        int below_lo = 0, below_hi = 0;
-        for (int i = lane; i < n_plan; i += 32) {
-            const int pg = block == 1 ? plan[i] / kPage : plan[i];
-            below_lo += pg < p.page_lo;
-            below_hi += pg < p.page_hi;
-        }
+    if (p.range_n > 0 && tid < 32) {
+        // plan entries per page range (this rank's share, or each fixed chunk of R21): the
+        // plan ascends, so range c holds entries [#(page < lo_c), #(page < hi_c))
+        for (int c = 0; c < p.range_n; ++c) {
+            const int plo = p.range_first + c * p.range_step, phi = plo + p.range_step;
+            int below_lo = 0, below_hi = 0;
+            for (int i = lane; i < n_plan; i += 32) {
+                const int pg = block == 1 ? plan[i] / kPage : plan[i];
+                below_lo += pg < plo;
+                below_hi += pg < phi;
+            }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            below_lo += __shfl_xor_sync(0xffffffffu, below_lo, off);
-            below_hi += __shfl_xor_sync(0xffffffffu, below_hi, off);
-        }
-        if (lane == 0) {
-            p.plan_lo[b] = below_lo;
-            p.plan_hi[b] = below_hi;
+            for (int off = 16; off > 0; off >>= 1) {
+                below_lo += __shfl_xor_sync(0xffffffffu, below_lo, off);
+                below_hi += __shfl_xor_sync(0xffffffffu, below_hi, off);
+            }
+            if (lane == 0) {
+                p.plan_lo[(size_t)c * p.max_batch + b] = below_lo;
+                p.plan_hi[(size_t)c * p.max_batch + b] = below_hi;
+            }
         }
     }
     if (tid == 0) {

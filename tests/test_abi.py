@@ -70,6 +70,9 @@ def test_tier_validation_matches_paper(ex):
     dict(num_full_prefix=3),                    # Delta layer 2 inside the full prefix
     dict(shard_world=2, shard_rank=2),          # rank outside [0, W)
     dict(shard_world=0),                        # W >= 1
+    dict(det_chunks=3, shard_world=2),          # R21: W | C
+    dict(det_chunks=-1),
+    dict(det_chunks=65),                        # C <= 64
 ])
 def test_config_errors(bad):
     with pytest.raises(DeltaError, match="CONFIG"):
@@ -82,7 +85,8 @@ def test_config_errors(bad):
     dict(select_layers=[], select_block=1),     # they work on pages
     dict(select_layers=[], kv_dtype=d200.DELTA_FP32),
     dict(select_layers=[], shard_world=2, shard_rank=0),
-], ids=["delta-layers", "token-mode", "fp32", "sharded"])
+    dict(select_layers=[], det_chunks=8),
+], ids=["delta-layers", "token-mode", "fp32", "sharded", "det-chunks"])
 def test_policy_config_errors(policy, bad):
     """Quest / RaaS restrictions are CONFIG errors (include/delta.h)."""
     with pytest.raises(DeltaError, match="CONFIG"):
@@ -119,3 +123,18 @@ def test_shard_ranges_partition_the_pages():
             assert got[0][0] == 0 and got[-1][1] == pages
             for (lo, hi), (lo2, _) in zip(got, got[1:]):
                 assert lo <= hi == lo2
+
+
+def test_det_chunk_ranges_are_unions_of_fixed_chunks():
+    """Host-only (R21): with det_chunks = C a rank's range is the union of its C/W consecutive
+    chunks of ceil(pages/C) pages — the same chunk boundaries for every W dividing C."""
+    C = 8
+    for max_seq in (16, 1000, 1600, 32768 + 64):
+        pages = -(-max_seq // 16)
+        per = -(-pages // C)
+        chunk = [(min(pages, c * per), min(pages, (c + 1) * per)) for c in range(C)]
+        for W in (1, 2, 4, 8):
+            got = [d200.shard_range(_c1(max_seq_len=max_seq, shard_world=W, shard_rank=r, det_chunks=C))
+                   for r in range(W)]
+            want = [(chunk[r * C // W][0], chunk[(r + 1) * C // W - 1][1]) for r in range(W)]
+            assert got == want, (max_seq, W)

@@ -38,7 +38,7 @@ def _exchange(st, which: int):
     ws[recv - base: recv - base + W * nbytes].copy_(torch.cat(parts).to(ws.device))
 
 
-def _worker(rank: int, port: int, q):
+def _worker(rank: int, port: int, q, det: int = 0):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -52,7 +52,7 @@ def _worker(rank: int, port: int, q):
         s, seed, B = 1500, 88, 2
         plant = planting_for(shape, s)
         cfg = shape.delta_config(B, 1600)
-        cfg.shard_world, cfg.shard_rank = W, rank
+        cfg.shard_world, cfg.shard_rank, cfg.det_chunks = W, rank, det
         bt = torch.from_numpy(synth.block_table(seed, B, cfg.max_pages))
         st = DeltaStack.allocate(cfg, bt)
         sd.fill_pools(st.kv_pool, st.block_table, seed, s - 1, B, range(shape.L), plant)
@@ -93,12 +93,13 @@ def _worker(rank: int, port: int, q):
         q.put(("err", f"rank {rank}: {e}\n{traceback.format_exc()}"))
 
 
-def test_two_process_sequence_sharding():
+@pytest.mark.parametrize("det", [0, 8], ids=["ranges", "r21-chunks"])
+def test_two_process_sequence_sharding(det):
     from helpers import GpuCase, Shape, assert_close_bf16, oracle_step, planting_for
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(W)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, det)) for r in range(W)]
     for p in procs:
         p.start()
     status, payload = q.get(timeout=600)
@@ -114,6 +115,13 @@ def test_two_process_sequence_sharding():
     plant = planting_for(shape, s)
     ref = GpuCase(shape, seed, batch=2, s_pre=s - 1, max_seq=1600, planting=plant)
     out_u, lse_u, plans_u = ref.step_layers(s)
+    if det:  # R21: bitwise equal to one process holding all 8 chunks
+        from test_gpu_shard import ShardedStack
+        one = ShardedStack(shape, seed, batch=2, s_pre=s - 1, max_seq=1600, W=1, planting=plant, det=det)
+        outs1, lses1, plans1 = one.step(*ref.inputs(s))
+        np.testing.assert_array_equal(out0, outs1[0])
+        np.testing.assert_array_equal(lse0, lses1[0])
+        assert [p.tolist() for p in plans0[1]] == [p.tolist() for p in plans1[1][0]]
     np.testing.assert_allclose(out0, out_u, atol=1e-5, rtol=0)
     np.testing.assert_allclose(lse0, lse_u, atol=1e-5, rtol=0)
     for b in range(2):
