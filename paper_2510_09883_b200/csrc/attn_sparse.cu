@@ -354,6 +354,9 @@ sparse_lat_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p)
         lp = p.plan_idx[e];
         phys = p.plan_phys[e];
     }
+    // the tiles' logical pages for the consumers, published by the CTA barrier below (the TMA
+    // barriers would order it too, but racecheck does not follow a tx-completed phase)
+    if (warp == 0 && lane < MT) tlp[lane] = lp;
     if (tid == 0) {
         for (int i = 0; i < MT; ++i) mbar_init(&bars[i], 1);
         cluster_stage_init<D>(cstage, p.gs);
@@ -374,8 +377,7 @@ sparse_lat_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p)
 #else
     if (warp == 0 && lane < n_items) {
 #endif
-        tlp[lane] = lp;
-        mbar_arrive_expect_tx(&bars[lane], kTile);  // release: tlp is visible to the waiter
+        mbar_arrive_expect_tx(&bars[lane], kTile);
         const int row0 = (int)kv_row((size_t)p.layer * p.num_phys + phys, p.g, h, 0);
         uint8_t* dst = tiles + lane * kTile;
         if (D == 64) tma_load_2d(dst, &tm_kv, &bars[lane], 0, row0, kEvictFirst);

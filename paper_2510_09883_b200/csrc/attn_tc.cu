@@ -90,8 +90,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
 
     if (tid == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
-            mbar_init(&full[i], TOKEN_PLAN ? 32 : 1);
-            mbar_init(&empty[i], NT);
+            mbar_init(&full[i], 32);  // every producer lane (it wrote row-token entries)
+            // every consumer LANE arrives on `empty` (and every producer lane on `full`): each
+            // lane reads / writes row-token entries of the stage, so each lane's accesses are
+            // ordered by its own release/acquire pair (one arrival per warp after __syncwarp is
+            // also correct under the PTX model, but racecheck does not follow the warp barrier)
+            mbar_init(&empty[i], NT * 32);
         }
         if (CL) cluster_stage_init<D>(cstage, p.gs);
         fence_mbar_init();
@@ -202,6 +206,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
                     const int phys_w = __shfl_sync(0xffffffffu, my_phys, j + (lane % NT));
                     __syncwarp();
                     if (lane == 0) mbar_arrive_expect_tx(&full[stg], valid * C::kTile);
+                    else mbar_arrive(&full[stg]);
                     __syncwarp();
                     if (lane < valid) {  // one 2P-row box: this head's K and V rows of the page
                         const int row0 = (int)kv_row(layer_ph + phys_w, p.g, h, 0);
@@ -444,8 +449,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
                 // generic-proxy smem writes must be ordered before the next TMA refill
                 if (wrote_smem) fence_proxy_async_smem();
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stg]);
+            mbar_arrive(&empty[stg]);
         }
 
         // ---------------------------------------------------------------- warp states
