@@ -339,6 +339,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
                 }
                 __syncwarp();
                 const uint32_t kt_u = smem_u32(kt), vt_u = smem_u32(vt);
+#ifndef EXP_TCNOMATH  // experiment builds: consumers skip the tile math (stream-only timing)
                 {
                 // ---- S^T = K Q^T: two accumulator chains (even / odd k-chunks)
                 float acc[NH][4], acc2[NH][4];
@@ -446,6 +447,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
                     }
                 }
                 }
+#else
+                (void)kt_u; (void)vt_u;
+#endif
                 // generic-proxy smem writes must be ordered before the next TMA refill
                 if (wrote_smem) fence_proxy_async_smem();
             }
