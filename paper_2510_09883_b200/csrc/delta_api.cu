@@ -334,6 +334,7 @@ struct delta_ctx {
     void* kv_pool = nullptr;
     const int32_t* block_table = nullptr;
     CUtensorMap tm_kv;
+    CUtensorMap tm_kvp;  // prefill: one box = 16 rows (K or V of a (page, head)) x one 64-column half
     bool use_tc = false;
     float scale = 0.f;
     std::vector<long long> step, dec_step, sel_step;
@@ -855,6 +856,13 @@ delta_status delta_create(const delta_config* cfg, const delta_buffers* bufs, de
         CUresult r = encode(&h->tm_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, bufs->kv_pool, dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        // prefill_umma.cu: the K rows and the V rows of a (page, head) as separate boxes, one
+        // 64-column half each, so 4 pages land as one uniformly strided [half][64 rows][128 B]
+        const cuuint32_t boxp[3] = {64, (cuuint32_t)kPage, 1};
+        if (r == CUDA_SUCCESS)
+            r = encode(&h->tm_kvp, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, bufs->kv_pool, dims, strides, boxp, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {
             delete h;
             return fail(nullptr, DELTA_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
@@ -1217,7 +1225,7 @@ delta_status delta_prefill(delta_t h, int32_t layer, int32_t batch, int32_t ntok
     p.q = q; p.kv_pool = h->kv_pool; p.block_table = h->block_table; p.seq_len = h->at<int32_t>(h->L.seq_len);
     p.out = out; p.lse_out = lse_out; p.err = h->at<int32_t>(h->L.err);
     // tcgen05 / TMEM kernel (prefill_umma.cu); the mma.sync kernel stays selectable (pfumma=0)
-    cudaError_t e = (h->tune_pfumma && prefill_umma_supported(p)) ? launch_prefill_umma(p, &h->tm_kv, stream, h->pdl)
+    cudaError_t e = (h->tune_pfumma && prefill_umma_supported(p)) ? launch_prefill_umma(p, &h->tm_kvp, stream, h->pdl)
                                                                   : launch_prefill(p, stream, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "prefill launch");
     ++h->launches;

@@ -11,15 +11,13 @@
 //   O[128 x D]  += P . V             per page: P_hi . V and P_lo . V, M=128 N=D K=16 (TMEM)
 // P enters as bf16 hi + lo (~16-bit probabilities, R18 as in the decode kernels).
 // Measured on this B200 (tools/umma_rate.cu): a tcgen05.mma costs ~46 cycles whatever its N up
-// to N = 32, 48 at N = 64 and 64 at N = 128 — so S is issued over 64-token blocks.  K rows of 4
-// pages are not uniformly strided in the pool (each (page, head) is K rows then V rows, 8 KiB),
-// so two copy warps restage the K rows of a block into one [half][64 rows][128 B] block (same
-// 128-byte swizzle phase: plain row copies); V stays in the TMA'd page (MN-major B operand).
-// Warps: 0-3 softmax + epilogue (thread = row), 4 TMA producer, 5 MMA issuer, 6-7 K restaging.
-// Measured (tools/prefill_bench.py): 246-292 TFLOP/s at the Llama-8B shape (the mma.sync kernel:
-// 142-186); ncu: the tensor pipe ~17 % busy, every role mostly waiting on the next — the chain
-// TMA -> restage -> S -> softmax -> PV -> slot release -> TMA is latency-bound.  Copying V out as
-// well (freeing each ring slot at once) with a single P buffer measured slower (250 TFLOP/s).
+// to N = 32, 48 at N = 64 and 64 at N = 128 — so S is issued over 64-token blocks.  The K rows
+// and the V rows of a block's 4 pages arrive as separate TMA boxes (16 rows x 128 B of one
+// 64-column half each: the pool interleaves K and V per (page, head), so only per-page boxes
+// give a uniformly strided [half][64 rows][128 B] operand) into their own 4-deep rings: a K
+// block is released by its S MMAs, a V block by its PV MMAs, and no warp copies operands.
+// Warps: 0-3 softmax + epilogue (thread = row), 4 K producer, 5 MMA issuer, 6 V producer (and
+// the zeroing of V rows past the end in the last page), 7 idle.
 #include <algorithm>
 
 #include "combine.cuh"
@@ -30,23 +28,22 @@ namespace {
 
 constexpr int kPuThreads = 256;
 constexpr int kPuKB = 4;                  // pages per KV block (64 tokens)
-constexpr int kPuNR = 8;                  // page slots in the TMA ring (two blocks)
+constexpr int kPuNB = 4;                  // blocks in the K ring and in the V ring
 constexpr int kPuBT = kPuKB * kPage;      // tokens per block
 constexpr float kPuRaise = 8.f;           // log2 headroom before the running max moves
 
 template <int D>
 struct PuCfg {
     static constexpr int kHalves = D / 64;
-    static constexpr int kTile = TileLayout<D>::kBytes;          // one (page, head): K rows then V rows
     static constexpr int kQ = kHalves * 128 * 128;               // Q: [half][128 rows][128 B]
-    static constexpr int kKst = kHalves * kPuBT * 128;           // K block: [half][64 rows][128 B]
+    static constexpr int kBlk = kHalves * kPuBT * 128;           // K or V block: [half][64 rows][128 B]
     static constexpr int kP = 128 * 128;                         // P: [128 rows][64 tok bf16]
     static constexpr int oQ = 0;
-    static constexpr int oRing = oQ + kQ;
-    static constexpr int oKst = oRing + kPuNR * kTile;           // 2 K blocks
-    static constexpr int oP = oKst + 2 * kKst;                   // 2 x (hi, lo)
+    static constexpr int oK = oQ + kQ;                           // K ring
+    static constexpr int oV = oK + kPuNB * kBlk;                 // V ring
+    static constexpr int oP = oV + kPuNB * kBlk;                 // 2 x (hi, lo)
     static constexpr int oBar = oP + 4 * kP;
-    static constexpr int nBar = 2 * kPuNR + 2 * 6;
+    static constexpr int nBar = 4 * kPuNB + 1 + 2 * 4;
     static constexpr int kSmem = 1024 + oBar + nBar * 8 + 16;
     static constexpr int kTmemCols = 256;                        // S: 2 x 64 columns, O: D columns at 128
     static constexpr int kOCol = 128;
@@ -59,14 +56,15 @@ prefill_umma_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPara
     extern __shared__ __align__(16) uint8_t pu_smem[];
     uint8_t* base = pu_smem + ((1024u - (smem_u32(pu_smem) & 1023u)) & 1023u);
     uint8_t* qs = base + C::oQ;
-    uint8_t* ring = base + C::oRing;
-    uint8_t* kst = base + C::oKst;
+    uint8_t* kring = base + C::oK;
+    uint8_t* vring = base + C::oV;
     uint8_t* pbuf = base + C::oP;  // [2][hi, lo][kP]
-    uint64_t* ring_full = reinterpret_cast<uint64_t*>(base + C::oBar);
-    uint64_t* ring_empty = ring_full + kPuNR;
-    uint64_t* kst_full = ring_empty + kPuNR;
-    uint64_t* kst_empty = kst_full + 2;
-    uint64_t* s_full = kst_empty + 2;
+    uint64_t* k_full = reinterpret_cast<uint64_t*>(base + C::oBar);
+    uint64_t* k_empty = k_full + kPuNB;
+    uint64_t* v_full = k_empty + kPuNB;
+    uint64_t* v_empty = v_full + kPuNB;
+    uint64_t* vz_done = v_empty + kPuNB;  // the last page's V rows past the end are zeroed
+    uint64_t* s_full = vz_done + 1;
     uint64_t* s_free = s_full + 2;
     uint64_t* p_full = s_free + 2;
     uint64_t* p_free = p_full + 2;
@@ -78,13 +76,14 @@ prefill_umma_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPara
     const int t0 = tile * T;
 
     if (tid == 0) {
-        for (int i = 0; i < kPuNR; ++i) {
-            mbar_init(&ring_full[i], 1);
-            mbar_init(&ring_empty[i], 1);  // the PV of the page completed
+        for (int i = 0; i < kPuNB; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);  // the block's S MMAs completed
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);  // the block's PV MMAs completed
         }
+        mbar_init(vz_done, 1);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&kst_full[i], 2);  // the two restaging warps
-            mbar_init(&kst_empty[i], 1);
             mbar_init(&s_full[i], 1);
             mbar_init(&s_free[i], 4);    // the four softmax warps
             mbar_init(&p_full[i], 4);
@@ -127,66 +126,62 @@ prefill_umma_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPara
     const size_t layer_ph = (size_t)p.layer * p.num_phys;
     const int32_t* bt = p.block_table + (size_t)b * p.bt_stride;
 
-    if (warp == 4) {
-        // ============================================================ TMA producer (pages in order)
+    // per block: the pages it holds and the TMA bytes of its K (or V) boxes
+    auto block_pages = [&](int i) { return min(kPuKB, n_pages - i * kPuKB); };
+    const bool tail = (kv_end % kPage) != 0;  // the last page holds rows past the end
+    if (warp == 4 || warp == 6) {
+        // ============================================================ TMA producers: K (warp 4)
+        // and V (warp 6), one 16-row box per (page, half) into the block's [half][64 rows][128 B]
+        const bool is_v = warp == 6;
+        uint8_t* ring = is_v ? vring : kring;
+        uint64_t* fullb = is_v ? v_full : k_full;
+        uint64_t* emptyb = is_v ? v_empty : k_empty;
         if (lane == 0) {
-            for (int pg = 0; pg < n_pages; ++pg) {
-                const int slot = pg % kPuNR, round = pg / kPuNR;
-                if (round > 0) mbar_wait(&ring_empty[slot], (round - 1) & 1);
-                mbar_arrive_expect_tx(&ring_full[slot], C::kTile);
-                const int row0 = (int)kv_row(layer_ph + bt[pg], p.g, h, 0);
-                uint8_t* dst = ring + slot * C::kTile;
-                if (D == 64) tma_load_2d(dst, &tm_kv, &ring_full[slot], 0, row0, kEvictNormal);
-                else tma_load_3d(dst, &tm_kv, &ring_full[slot], 0, row0, 0, kEvictNormal);
-            }
-        }
-    } else if (warp >= 6) {
-        // ============================================================ K restaging (64 threads)
-        const int ct = tid - 192;
-        for (int i = 0; i < nblk; ++i) {
-            if (i >= 2) mbar_wait(&kst_empty[i & 1], ((i - 2) >> 1) & 1);
-            uint8_t* kb = kst + (i & 1) * C::kKst;
-            for (int q = 0; q < kPuKB; ++q) {
-                const int pg = i * kPuKB + q;
-                if (pg >= n_pages) break;
-                const int slot = pg % kPuNR;
-                mbar_wait(&ring_full[slot], (pg / kPuNR) & 1);
-                const uint8_t* src = ring + slot * C::kTile;
-                // 16 K rows x 128 B per half: 128 chunks per half, 2 per thread per half; the rows
-                // keep their 128-byte swizzle phase (row % 8)
+            for (int i = 0; i < nblk; ++i) {
+                const int slot = i % kPuNB, round = i / kPuNB;
+                if (round > 0) mbar_wait(&emptyb[slot], (round - 1) & 1);
+                const int np = block_pages(i);
+                mbar_arrive_expect_tx(&fullb[slot], np * C::kHalves * kPage * 128);
+                for (int q = 0; q < np; ++q) {
+                    const int row0 = (int)kv_row(layer_ph + bt[i * kPuKB + q], p.g, h, 0) + (is_v ? kPage : 0);
 #pragma unroll
-                for (int hf = 0; hf < C::kHalves; ++hf)
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int ch = ct + 64 * u, row = ch >> 3, c16 = ch & 7;
-                        const uint4 v = *reinterpret_cast<const uint4*>(src + hf * TileLayout<D>::kHalfBytes + row * 128 + c16 * 16);
-                        *reinterpret_cast<uint4*>(kb + hf * (kPuBT * 128) + (q * kPage + row) * 128 + c16 * 16) = v;
-                    }
-                if (pg == n_pages - 1 && kv_end % kPage) {  // partial last page: zero V rows past the end
-                    const int r0 = kv_end % kPage;
-                    uint8_t* vt = ring + slot * C::kTile + TileLayout<D>::kVOff;
-                    for (int ch = ct; ch < (kPage - r0) * (D / 8); ch += 64) {
-                        const int r = r0 + ch / (D / 8), c = ch % (D / 8);
-                        *reinterpret_cast<uint4*>(vt + swz<D>(r, c)) = make_uint4(0, 0, 0, 0);  // 0 * garbage != NaN
+                    for (int hf = 0; hf < C::kHalves; ++hf) {
+                        uint8_t* dst = ring + slot * C::kBlk + hf * (kPuBT * 128) + q * kPage * 128;
+                        if (D == 64) tma_load_2d(dst, &tm_kv, &fullb[slot], 0, row0, kEvictNormal);
+                        else tma_load_3d(dst, &tm_kv, &fullb[slot], 0, row0, hf, kEvictNormal);
                     }
                 }
             }
+        }
+        // (a parity wait names one of two phases: the other lanes may wait for the last block only
+        // once lane 0 has issued it, i.e. its slot's barrier is in that block's phase)
+        __syncwarp();
+        if (is_v && tail && nblk > 0) {
+            // V rows past the end in the last page: 0 (P is 0 there, but 0 * garbage may be NaN)
+            const int i = nblk - 1, slot = i % kPuNB, q = block_pages(i) - 1, r0 = kv_end % kPage;
+            mbar_wait(&v_full[slot], (i / kPuNB) & 1);
+            uint8_t* vb = vring + slot * C::kBlk;
+            for (int ch = lane; ch < C::kHalves * (kPage - r0) * 8; ch += 32) {
+                const int hf = ch / ((kPage - r0) * 8), rem = ch - hf * (kPage - r0) * 8;
+                const int r = q * kPage + r0 + rem / 8, c = rem % 8;
+                *reinterpret_cast<uint4*>(vb + hf * (kPuBT * 128) + r * 128 + ((c ^ (r & 7)) << 4)) = make_uint4(0, 0, 0, 0);
+            }
             fence_proxy_async_smem();  // generic stores -> the tensor core's async-proxy reads
             __syncwarp();
-            if (lane == 0) mbar_arrive(&kst_full[i & 1]);
+            if (lane == 0) mbar_arrive(vz_done);
         }
     } else if (warp == 5) {
         // ============================================================ MMA issuer (one lane)
         constexpr uint32_t kIdS = umma_idesc(128, kPuBT, 0, 0);  // A = Q K-major, B = K rows K-major
         constexpr uint32_t kIdPV = umma_idesc(128, D, 0, 1);     // A = P K-major, B = V MN-major
-        const uint32_t qs_u = smem_u32(qs), kst_u = smem_u32(kst), ring_u = smem_u32(ring), p_u = smem_u32(pbuf);
+        const uint32_t qs_u = smem_u32(qs), k_u = smem_u32(kring), v_u = smem_u32(vring), p_u = smem_u32(pbuf);
         for (int i = 0; i <= nblk; ++i) {
             if (i < nblk) {  // S(i)
-                mbar_wait(&kst_full[i & 1], (i >> 1) & 1);
+                mbar_wait(&k_full[i % kPuNB], (i / kPuNB) & 1);
                 if (i >= 2) mbar_wait(&s_free[i & 1], ((i - 2) >> 1) & 1);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t kb = kst_u + (i & 1) * C::kKst;
+                    const uint32_t kb = k_u + (i % kPuNB) * C::kBlk;
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
                         const uint64_t a = umma_desc(qs_u + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, kLayoutSW128);
@@ -194,34 +189,34 @@ prefill_umma_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPara
                         umma(tbase + (i & 1) * kPuBT, a, bk, kIdS, kk > 0 ? 1u : 0u);
                     }
                     umma_commit(&s_full[i & 1]);
-                    umma_commit(&kst_empty[i & 1]);
+                    umma_commit(&k_empty[i % kPuNB]);
                 }
                 __syncwarp();
             }
             if (i >= 1) {  // PV(i - 1), after its softmax wrote P
                 const int j = i - 1;
                 mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+                mbar_wait(&v_full[j % kPuNB], (j / kPuNB) & 1);
+                if (tail && j == nblk - 1) mbar_wait(vz_done, 0);
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t ph = p_u + (j & 1) * 2 * C::kP, pl = ph + C::kP;
-                    for (int q = 0; q < kPuKB; ++q) {
-                        const int pg = j * kPuKB + q;
-                        if (pg >= n_pages) break;
-                        const int slot = pg % kPuNR;
-                        // V rows of the page in its ring slot: MN-major, halves kHalfBytes apart
-                        const uint64_t bv = umma_desc(ring_u + slot * C::kTile + TileLayout<D>::kVOff,
-                                                      D == 128 ? TileLayout<D>::kHalfBytes : 0, 1024, kLayoutSW128);
+                    const uint32_t vb = v_u + (j % kPuNB) * C::kBlk;
+                    const int np = block_pages(j);
+                    for (int q = 0; q < np; ++q) {
+                        // V rows of page q: MN-major, the two d halves kPuBT * 128 bytes apart
+                        const uint64_t bv = umma_desc(vb + q * kPage * 128, D == 128 ? kPuBT * 128 : 0, 1024, kLayoutSW128);
                         umma(tbase + C::kOCol, umma_desc(ph + q * 32, 16, 1024, kLayoutSW128), bv, kIdPV,
                              (j > 0 || q > 0) ? 1u : 0u);
                         umma(tbase + C::kOCol, umma_desc(pl + q * 32, 16, 1024, kLayoutSW128), bv, kIdPV, 1u);
-                        umma_commit(&ring_empty[slot]);
                     }
+                    umma_commit(&v_empty[j % kPuNB]);
                     umma_commit(&p_free[j & 1]);
                 }
                 __syncwarp();
             }
         }
-    } else {
+    } else if (warp < 4) {
         // ============================================================ softmax (thread = row)
         const int r = tid, j = r / T, i_tok = r - j * T;
         const bool valid = j < gs && t0 + i_tok < p.ntok;
