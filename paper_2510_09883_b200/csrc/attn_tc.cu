@@ -127,6 +127,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     const int32_t* plan_phys = p.plan_phys + (size_t)b * p.plan_cap;
     const size_t layer_ph = (size_t)p.layer * p.num_phys;
     if (p.prewait && warp != NCW) pdl_wait();
+    if (!CL && p.gll && tid == 0) sflag[0] = (int)ll_flag(p, b, h, p.nsplit);  // after the wait (combine.cuh)
     // Every CTA has passed its wait here (the producer never reads upstream outputs), so the
     // previous kernel is complete: let the next layer's kernel launch now — its CTAs co-reside
     // (two per SM), resolve their geometry and start their KV stream during this kernel.
@@ -492,7 +493,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     if (tid == 0) DTRACE(4);
     if (CL) cluster_epilogue<D, NCW, OSR>(p, ms, ls, os, cstage, b, h, stale, cap_err, s);
     else global_epilogue<D, NCW, OSR>(p, ms, ls, os, reinterpret_cast<float*>(ring) + kMergeScratch, b, h, split,
-                                       stale, cap_err, s);
+                                       stale, cap_err, s, (uint32_t)sflag[0]);
     if (tid == 0) DTRACE(6);
 }
 

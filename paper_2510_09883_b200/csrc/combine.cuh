@@ -352,10 +352,38 @@ __device__ __forceinline__ void st_release_gpu(int32_t* a, int v) {
     asm volatile("st.release.gpu.s32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
 
+// Low-latency (LL) words of the gmerge partials (AttnParams::gll): every 8-byte word carries
+// (value, flag), written by one 8-byte-aligned store (single-copy atomic), so a reader that sees
+// the flag of this launch also sees the value — the merging CTAs poll the partials themselves
+// instead of drawing a ticket, waiting for the last one and then loading (two global round trips
+// fewer on the critical path).  The flag identifies the launch: ((E + 1) << 6) | (ns - 1) with
+// E = floor(gcnt[b][h][ns - 1] / ns) read after griddepcontrol.wait (every CTA adds 1 to that
+// counter with a fire-and-forget red, so E is the same for all CTAs of a launch whichever has
+// already added, and grows by one per launch with this split count).
+__device__ __forceinline__ void st_ll2(void* a, float v0, float v1, uint32_t f) {
+    asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a), "r"(__float_as_uint(v0)), "r"(f),
+                 "r"(__float_as_uint(v1)), "r"(f)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 ld_ll2(const void* a) {
+    uint4 r;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(a)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ uint32_t ll_flag(const AttnParams& p, int b, int h, int ns) {
+    const unsigned long long* cnt = p.gcnt + ((size_t)b * p.g + h) * kMaxSplitG + (ns - 1);
+    unsigned long long c;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(c) : "l"(cnt) : "memory");
+    return (uint32_t)(((c / (unsigned long long)ns + 1ull) << 6) | (unsigned long long)(ns - 1));
+}
+
 template <int D, int NW, int OSROWS>
 __device__ __forceinline__ void global_epilogue(const AttnParams& p, const float* ms, const float* ls,
                                                 const float* os, float* scratch, int b, int h, int split,
-                                                bool stale, bool cap_err, int s_post) {
+                                                bool stale, bool cap_err, int s_post, uint32_t llf = 0) {
     const int tid = threadIdx.x, nthreads = blockDim.x;
     const int gs = p.gs, ns = p.nsplit;
     constexpr int C4 = D / 4, OS = os_stride<D>();
@@ -408,12 +436,47 @@ __device__ __forceinline__ void global_epilogue(const AttnParams& p, const float
         }
         if (ns == 1) {
             emit(row, c4, M, L, o);
+        } else if (p.gll) {  // LL words: slot of 2 * gpart_floats words (value, flag)
+            uint32_t* w = reinterpret_cast<uint32_t*>(p.gpart) + (((size_t)b * p.g + h) * ns + split) * 2 * rec;
+            st_ll2(w + ((size_t)row * D + c4 * 4) * 2, o.x, o.y, llf);
+            st_ll2(w + ((size_t)row * D + c4 * 4 + 2) * 2, o.z, o.w, llf);
+            if (c4 == 0) st_ll2(w + ((size_t)kMaxGs * D + 2 * row) * 2, M, L, llf);
         } else {
             reinterpret_cast<float4*>(my + (size_t)row * D)[c4] = o;
             if (c4 == 0) reinterpret_cast<float2*>(my + kMaxGs * D)[row] = make_float2(M, L);
         }
     }
-    if (ns > 1) {
+    if (ns > 1 && p.gll) {
+        // 2'. this launch's ticket (fire and forget: only keeps the epoch counter moving), then
+        //     poll this CTA's slice of the ns partials until every word carries this launch's flag
+        if (tid == 0) {
+            unsigned long long* cnt = p.gcnt + ((size_t)b * p.g + h) * kMaxSplitG + (ns - 1);
+            asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(cnt) : "memory");
+        }
+        const int per = (total + ns - 1) / ns, lo = split * per, n = max(0, min(total, lo + per) - lo);
+        const uint32_t* wb = reinterpret_cast<const uint32_t*>(p.gpart) + ((size_t)b * p.g + h) * ns * 2 * rec;
+        float4* sx = reinterpret_cast<float4*>(scratch);
+        float2* sml = reinterpret_cast<float2*>(sx + per * ns);
+        for (int i = tid; i < n * ns; i += nthreads) {
+            const int k = i / ns, c = i - k * ns;
+            const int idx = lo + k, row = idx / C4, c4 = idx - row * C4;
+            const uint32_t* w = wb + (size_t)c * 2 * rec;
+            const uint32_t* a0 = w + ((size_t)row * D + c4 * 4) * 2;
+            const uint32_t* a2 = w + ((kMaxGs * D) + 2 * row) * 2;
+            uint4 x0, x1, y;
+            do {
+                x0 = ld_ll2(a0);
+                x1 = ld_ll2(a0 + 4);
+                y = ld_ll2(a2);
+            } while (x0.y != llf || x0.w != llf || x1.y != llf || x1.w != llf || y.y != llf || y.w != llf);
+            sx[i] = make_float4(__uint_as_float(x0.x), __uint_as_float(x0.z), __uint_as_float(x1.x),
+                                __uint_as_float(x1.z));
+            sml[i] = make_float2(__uint_as_float(y.x), __uint_as_float(y.z));
+        }
+        __syncthreads();
+        if (tid == 0) DTRACE(9);
+    }
+    if (ns > 1 && !p.gll) {
         // 2. arrive (ticket on the (b, h, ns) 64-bit counter: launches with this split count
         //    always add exactly ns, so the counter is a multiple of ns between launches) and
         //    wait until all ns tickets of this launch are drawn
@@ -444,6 +507,11 @@ __device__ __forceinline__ void global_epilogue(const AttnParams& p, const float
         }
         __syncthreads();
         if (tid == 0) DTRACE(9);
+    }
+    if (ns > 1) {
+        const int per = (total + ns - 1) / ns, lo = split * per, n = max(0, min(total, lo + per) - lo);
+        const float4* sx = reinterpret_cast<const float4*>(scratch);
+        const float2* sml = reinterpret_cast<const float2*>(sx + per * ns);
         const int lane = tid & 31, warp = tid >> 5, nwarps = nthreads >> 5;
         for (int k = warp; k < n; k += nwarps) {
             const int idx = lo + k, row = idx / C4, c4 = idx - row * C4;

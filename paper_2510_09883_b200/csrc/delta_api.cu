@@ -236,7 +236,7 @@ Layout layout(const delta_config& c, int sms) {
     L.stage_v = take(2 * (size_t)c.num_layers * c.max_batch * g * D * e);
     L.stage_out = take(2 * (size_t)c.num_layers * c.max_batch * m * D * 4);
     L.gslots = std::max(sms, 1) * 2;  // batch * g * nsplit <= sms for every gmerge launch
-    L.gpart = take((size_t)L.gslots * gpart_floats(D) * 4);
+    L.gpart = take((size_t)L.gslots * gpart_floats(D) * 8);  // LL words (value, flag) with gll
     L.gcnt = take((size_t)c.max_batch * g * kMaxSplitG * 8);  // ticket counter per (b, h, split count)
     {   // Quest page representatives [L][num_phys][g][2][d] bf16
         const long long phys = c.num_phys_pages > 0 ? c.num_phys_pages : (long long)c.max_batch * L.max_pages;
@@ -361,7 +361,7 @@ struct delta_ctx {
     // cycles to issue (tools/umma_test.cu), so 10 per tile lose to the mma.sync kernel here;
     // kept selectable (DELTA_TUNE umma=1) and parity-tested.
     int tune_prewait = 1, tune_early = 1, tune_umma = 0, tune_policy = 0;
-    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1, tune_gm2 = 0, tune_lat = 1, tune_qpf = 1, tune_pfumma = 1;
+    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1, tune_gm2 = 0, tune_lat = 1, tune_qpf = 1, tune_pfumma = 1, tune_gll = 1;
     // sequence sharding
     int world = 1, rank = 0, page_lo = 0, page_hi = 0x7fffffff;
     ncclComm_t comm = nullptr;  // null with world > 1: the caller exchanges (delta_shard_* calls)
@@ -445,6 +445,7 @@ AttnParams attn_params(delta_ctx* h, int layer, int batch, int role_override = -
         p.gpart = h->at<float>(h->L.gpart);
         p.gcnt = h->at<unsigned long long>(h->L.gcnt);
         p.gm_shallow = h->tune_gm2;
+        p.gll = h->tune_gll;
     }
     const int cap = p.gmerge ? std::min(kMaxSplitG, h->L.gslots / std::max(1, batch * c.num_kv_heads)) : kMaxSplit;
     if (h->tune_nsplit > 0) p.nsplit = std::min(h->tune_nsplit, cap);
@@ -1336,7 +1337,7 @@ delta_status delta_set_tuning(delta_t h, const char* key, int32_t value) {
         {"nsplit", &h->tune_nsplit}, {"snsplit", &h->tune_snsplit}, {"deep", &h->tune_deep},
         {"prewait", &h->tune_prewait}, {"early", &h->tune_early}, {"umma", &h->tune_umma},
         {"policy", &h->tune_policy}, {"seltrig", &h->tune_seltrig}, {"selhist", &h->tune_selhist},
-        {"gmerge", &h->tune_gmerge}, {"gm2", &h->tune_gm2}, {"lat", &h->tune_lat}, {"qpf", &h->tune_qpf}, {"pfumma", &h->tune_pfumma}};
+        {"gmerge", &h->tune_gmerge}, {"gm2", &h->tune_gm2}, {"lat", &h->tune_lat}, {"qpf", &h->tune_qpf}, {"pfumma", &h->tune_pfumma}, {"gll", &h->tune_gll}};
     for (const Knob& k : knobs)
         if (std::strcmp(k.name, key) == 0) {
             *k.field = value;
