@@ -50,7 +50,7 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
-    size_t seq_len, err, cnt_sel, logits, lse_buf, keys, plan_idx, plan_phys, plan_count, plan_stamp, plan_lo, plan_hi,
+    size_t seq_len, err, cnt_sel, sel_epoch, keys_ll, logits, lse_buf, keys, plan_idx, plan_phys, plan_count, plan_stamp, plan_lo, plan_hi,
         shard_send, shard_recv, cand_send, cand_recv, stage_q, stage_k, stage_v, stage_out, gpart, gcnt, reps, ticket,
         raas_last,
         reps_bytes, total;
@@ -207,6 +207,8 @@ Layout layout(const delta_config& c, int sms) {
     L.logits = take(has_sel ? (size_t)c.max_batch * c.max_seq_len * m * 4 : 0);
     L.lse_buf = take((size_t)c.max_batch * m * 4);
     L.keys = take(has_sel ? (size_t)c.max_batch * L.max_units * 4 : 0);
+    L.keys_ll = take(has_sel ? (size_t)c.max_batch * L.max_units * 8 : 0);
+    L.sel_epoch = take((size_t)c.num_layers * c.max_batch * 4);
     // plan slots: one per Delta layer; QUEST: slot 0 = the current layer's plan; RAAS: one per layer
     const int nd = c.policy == DELTA_POLICY_RAAS ? c.num_layers : std::max(1, L.n_delta);
     L.plan_idx = take((size_t)nd * c.max_batch * L.plan_cap * 4);
@@ -361,7 +363,7 @@ struct delta_ctx {
     // cycles to issue (tools/umma_test.cu), so 10 per tile lose to the mma.sync kernel here;
     // kept selectable (DELTA_TUNE umma=1) and parity-tested.
     int tune_prewait = 1, tune_early = 1, tune_umma = 0, tune_policy = 0;
-    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1, tune_gm2 = 0, tune_lat = 1, tune_qpf = 1, tune_pfumma = 1, tune_gll = 1;
+    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1, tune_gm2 = 0, tune_lat = 1, tune_qpf = 1, tune_pfumma = 1, tune_gll = 1, tune_selll = 1;
     // sequence sharding
     int world = 1, rank = 0, page_lo = 0, page_hi = 0x7fffffff;
     ncclComm_t comm = nullptr;  // null with world > 1: the caller exchanges (delta_shard_* calls)
@@ -692,6 +694,9 @@ delta_status launch_sel(delta_ctx* h, int layer, int batch, const float* keys_ov
     p.plan_stamp = h->at<int32_t>(h->L.plan_stamp) + (size_t)sl * c.max_batch;
     p.idx_out = idx_out; p.count_out = count_out;
     p.cnt = h->at<int32_t>(h->L.cnt_sel) + (size_t)layer * c.max_batch;
+    p.ll = (h->tune_selll && shard_mode == 0 && !keys_override && !k_new && h->L.max_units <= kSelSmemUnits) ? 1 : 0;
+    p.keys_ll = h->at<uint2>(h->L.keys_ll);
+    p.epoch = h->at<int32_t>(h->L.sel_epoch);  // one epoch per sequence: keys_ll is shared by the layers
     p.shard_mode = shard_mode;
     p.page_lo = h->page_lo; p.page_hi = h->page_hi;
     p.cand_out = h->at<uint2>(h->L.cand_send);
@@ -1337,7 +1342,7 @@ delta_status delta_set_tuning(delta_t h, const char* key, int32_t value) {
         {"nsplit", &h->tune_nsplit}, {"snsplit", &h->tune_snsplit}, {"deep", &h->tune_deep},
         {"prewait", &h->tune_prewait}, {"early", &h->tune_early}, {"umma", &h->tune_umma},
         {"policy", &h->tune_policy}, {"seltrig", &h->tune_seltrig}, {"selhist", &h->tune_selhist},
-        {"gmerge", &h->tune_gmerge}, {"gm2", &h->tune_gm2}, {"lat", &h->tune_lat}, {"qpf", &h->tune_qpf}, {"pfumma", &h->tune_pfumma}, {"gll", &h->tune_gll}};
+        {"gmerge", &h->tune_gmerge}, {"gm2", &h->tune_gm2}, {"lat", &h->tune_lat}, {"qpf", &h->tune_qpf}, {"pfumma", &h->tune_pfumma}, {"gll", &h->tune_gll}, {"selll", &h->tune_selll}};
     for (const Knob& k : knobs)
         if (std::strcmp(k.name, key) == 0) {
             *k.field = value;

@@ -33,6 +33,7 @@ enum DevErr : int { kDevOk = 0, kDevUsage = 2, kDevNumeric = 3, kDevCapacity = 4
 constexpr int kPage = 16;        // P
 constexpr int kMaxGs = 16;       // query heads per KV group handled by one MMA row tile
 constexpr int kMaxSplit = 16;    // split-K CTAs per (sequence, kv head) = one thread-block cluster
+constexpr int kSelSmemUnits = 16384;  // select: unit keys cached in shared memory up to this many
 constexpr int kMaxSplitG = 64;   // split-K CTAs per (sequence, kv head) with the global merge
 // Floats of one split's partial in the global-merge buffer: O rows [kMaxGs][d] then (M, L) pairs.
 __host__ __device__ constexpr int gpart_floats(int d) { return kMaxGs * d + 2 * kMaxGs; }
@@ -115,6 +116,11 @@ struct SelectParams {
     int32_t* idx_out;           // optional [batch][plan_cap]
     int32_t* count_out;         // optional [batch]
     int32_t* cnt;               // [max_batch] arrival counters (this layer)
+    // LL hand-off (ll = 1): phase-A CTAs also publish each unit key as a (key bits, flag) word;
+    // CTA 0 polls them instead of an arrival election (flag = epoch[b] + 1, epoch bumped by CTA 0)
+    int ll;
+    uint2* keys_ll;             // [max_batch][max_units]
+    int32_t* epoch;             // [max_batch] (every layer: the flags must differ across layers too)
     int32_t* err;
     // sequence sharding: mode 0 = unsharded; 1 = local (keys of own units only; export the
     // rank's top-k candidates to cand_out); 2 = global merge (keys_override = the dense keys

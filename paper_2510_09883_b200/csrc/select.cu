@@ -47,6 +47,22 @@ constexpr int kSelThreads = DELTA_SEL_THREADS;  // 1024 measured: C1 select 10.8
 constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kSmemUnits = 16384;  // keys cached in shared memory up to this many units
 
+// LL unit keys (SelectParams::ll): one 8-byte (key bits, flag) word per unit, single-copy atomic
+__device__ __forceinline__ void st_key_ll(uint2* a, float key, uint32_t flag) {
+    asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1, %2};" ::"l"(a), "r"(__float_as_uint(key)), "r"(flag)
+                 : "memory");
+}
+__device__ __forceinline__ uint2 ld_key_ll(const uint2* a) {
+    uint2 w;
+    asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y) : "l"(a) : "memory");
+    return w;
+}
+__device__ __forceinline__ float poll_key_ll(const uint2* a, uint32_t flag) {
+    uint2 w = ld_key_ll(a);
+    while (w.y != flag) w = ld_key_ll(a);
+    return __uint_as_float(w.x);
+}
+
 __device__ __forceinline__ uint32_t key_bits(float f) {
     f = (f == 0.0f) ? 0.0f : f;  // -0 and +0 rank equal
     const uint32_t u = __float_as_uint(f);
@@ -154,7 +170,7 @@ __device__ __forceinline__ int topk_regs(const SelectParams& p, int n_units, int
                                       const float* __restrict__ src, const int32_t* __restrict__ bt,
                                       int32_t* plan, int32_t* plan_phys, uint32_t* sm_keys, int* hist2,
                                       int* scratch, uint32_t& s_and, uint32_t& s_or, int& s_bin, int& s_rem,
-                                      int& s_cnt) {
+                                      int& s_cnt, const uint2* kll, uint32_t llf) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     auto forced = [&](int u) { return u < sink_hi || u >= win_lo; };
     auto phys_of = [&](int u) -> int32_t { return block == 1 ? bt[u / kPage] * kPage + (u % kPage) : bt[u]; };
@@ -169,11 +185,25 @@ __device__ __forceinline__ int topk_regs(const SelectParams& p, int n_units, int
     uint32_t* s_key = sm_keys;                                                  // [n_units]
     int32_t* s_phys = reinterpret_cast<int32_t*>(sm_keys + n_units);            // [n_units]
     bool bad = false;
+    uint2 w[IPT];  // LL: one round of independent loads, then re-poll the words not yet published
+    if (kll) {
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const int u = i * kSelThreads + tid;
+            if (u < n_units) w[i] = ld_key_ll(kll + u);
+        }
+    }
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
         const int u = i * kSelThreads + tid;
         if (u < n_units) {
-            const float f = __ldcg(src + u);
+            float f;
+            if (kll) {
+                while (w[i].y != llf) w[i] = ld_key_ll(kll + u);
+                f = __uint_as_float(w[i].x);
+            } else {
+                f = __ldcg(src + u);
+            }
             s_key[u] = key_bits(f);
             s_phys[u] = phys_of(u);
             bad |= isnan(f);
@@ -328,10 +358,16 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
     // the length load, ~2800 for the LSE + logits, against ~300 for an uncontended L2 hit)
     __shared__ int s_len;
     __shared__ __align__(16) float s_lse[256];
-    if (tid == 0) s_len = p.seq_len[p.layer * p.max_batch + b];
+    __shared__ uint32_t s_llf;
+    if (tid == 0) {
+        s_len = p.seq_len[p.layer * p.max_batch + b];
+        if (p.ll) s_llf = (uint32_t)p.epoch[b] + 1u;  // this launch's LL flag (same round trip)
+    }
     if (!p.keys_override && !p.k_new && tid < p.m) s_lse[tid] = p.lse_buf[(size_t)b * p.m + tid];
     __syncthreads();
     int s = s_len / p.g;  // raw counter = n * g
+    const uint32_t llf = p.ll ? s_llf : 0u;
+    const uint2* kll = p.ll ? p.keys_ll + (size_t)b * p.max_units : nullptr;
     if (p.k_new) {
         // Quest layer: Eq.7 append of this step's token at position s, then
         // fold it into its page's min/max representatives (quest.cu); a token in slot 0 starts
@@ -414,7 +450,11 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
                 float sum = 0.f;
 #pragma unroll
                 for (int r = 0; r < kPage; ++r) sum += __shfl_sync(0xffffffffu, e, 2 * r);  // ascending t
-                if (lane == 0) keys_b[u] = (u * kPage >= own_lo && u * kPage < own_hi) ? sum : -INFINITY;
+                if (lane == 0) {
+                    const float key = (u * kPage >= own_lo && u * kPage < own_hi) ? sum : -INFINITY;
+                    keys_b[u] = key;
+                    if (p.ll) st_key_ll(p.keys_ll + (size_t)b * p.max_units + u, key, llf);
+                }
                 if (u == u_lo + warp) SELCLK(3);
             }
         } else {
@@ -425,13 +465,21 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
                 float mx = -INFINITY;
                 if (t < t_hi && own) mx = head_max(lg + (size_t)t * p.m, lsl, lse_g, p.m, hh);
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-                if (t < t_hi && hh == 0) keys_b[t] = mx;
+                if (t < t_hi && hh == 0) {
+                    keys_b[t] = mx;
+                    if (p.ll) st_key_ll(p.keys_ll + (size_t)b * p.max_units + t, mx, llf);
+                }
             }
         }
         // arrival: the barrier puts every thread's key stores before thread 0's acq_rel atomic
         // (release, cumulative); the last arrival's acquire + the barrier order its threads'
         // key loads after every other CTA's stores — no per-thread fences
         SELCLK(4);
+        if (p.ll) {  // LL hand-off: CTA 0 ranks, polling the published keys; the others are done
+            if (blockIdx.x != 0) return;
+            if (tid == 0) DTRACE(2);
+            goto phase_b;
+        }
         __syncthreads();
         if (tid == 0) DTRACE(2);
         if (tid == 0) {
@@ -450,6 +498,7 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
     }
 
     // ------------------------------------------------------------ phase B: top-k
+phase_b:
     int32_t* plan = p.plan_idx + (size_t)b * p.plan_cap;
     int32_t* plan_phys = p.plan_phys + (size_t)b * p.plan_cap;
     const int32_t* bt = p.block_table + (size_t)b * p.bt_stride;
@@ -470,6 +519,8 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
     }
 
     if (n_cand <= p.k_units) {
+        if (kll)  // the epoch may only move once every phase-A CTA has published (hence read it)
+            for (int u = tid; u < n_units; u += kSelThreads) (void)poll_key_ll(kll + u, llf);
         for (int u = tid; u < n_units; u += kSelThreads) {  // R12: budget covers all
             plan[u] = u;
             plan_phys[u] = phys_of(u);
@@ -479,19 +530,19 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
         const int ipt = (n_units + kSelThreads - 1) / kSelThreads;
         if (ipt <= 4)
             count = topk_regs<4>(p, n_units, sink_hi, win_lo, block, src, bt, plan, plan_phys, sm_keys, hist2,
-                                 scratch, s_and, s_or, s_bin, s_rem, s_cnt);
+                                 scratch, s_and, s_or, s_bin, s_rem, s_cnt, kll, llf);
         else if (ipt <= 8)
             count = topk_regs<8>(p, n_units, sink_hi, win_lo, block, src, bt, plan, plan_phys, sm_keys, hist2,
-                                 scratch, s_and, s_or, s_bin, s_rem, s_cnt);
+                                 scratch, s_and, s_or, s_bin, s_rem, s_cnt, kll, llf);
         else
             count = topk_regs<16>(p, n_units, sink_hi, win_lo, block, src, bt, plan, plan_phys, sm_keys, hist2,
-                                  scratch, s_and, s_or, s_bin, s_rem, s_cnt);
+                                  scratch, s_and, s_or, s_bin, s_rem, s_cnt, kll, llf);
     } else {
         const bool cached = n_units <= kSmemUnits;
         bool bad = false;
         if (cached) {
             for (int u = tid; u < n_units; u += kSelThreads) {
-                const float f = __ldcg(src + u);
+                const float f = kll ? poll_key_ll(kll + u, llf) : __ldcg(src + u);
                 bad |= isnan(f);
                 sm_keys[u] = key_bits(f);
             }
@@ -698,6 +749,7 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
         }
     }
     if (tid == 0) {
+        if (kll) p.epoch[b] = (int32_t)llf;  // every phase-A CTA has read the old epoch
         p.plan_count[b] = n_plan;
         p.plan_stamp[b] = s;
         if (p.count_out) p.count_out[b] = n_plan;
