@@ -476,8 +476,9 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
         // key loads after every other CTA's stores — no per-thread fences
         SELCLK(4);
         if (p.ll) {  // LL hand-off: CTA 0 ranks, polling the published keys; the others are done
-            if (blockIdx.x != 0) return;
+            SELCLK(5);
             if (tid == 0) DTRACE(2);
+            if (blockIdx.x != 0) return;
             goto phase_b;
         }
         __syncthreads();
