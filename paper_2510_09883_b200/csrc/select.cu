@@ -297,6 +297,11 @@ __device__ __forceinline__ int topk_regs(const SelectParams& p, int n_units, int
         remaining = rem;
         bin_cnt = cnt;
         if (tid == 0) DTRACE(7 + pass);
+        // every candidate of the bin is taken: T = the bin's lowest key image (prefix, low bits
+        // 0), so {key > T} U {key == T} is exactly the higher bins plus this whole bin — the
+        // remaining digits cannot change the selection (typically after the second digit, where
+        // the k-th key's bin holds that key alone)
+        if (cnt == rem) break;
     }
     if (tid == 0) DTRACE(4);
     // selection: forced, key > T, and the lowest-index `remaining` of the keys == T
