@@ -336,9 +336,355 @@ prefill_umma_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPara
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::kTmemCols));
 }
 
+// ================================================================================================
+// Operands in TMEM (pfumma = 2): Q and P are the A operands of the two MMAs, and both live in
+// tensor memory instead of shared memory — tcgen05.mma [d], [a_tmem], b_desc — so the tensor
+// core reads only K (for S) and V (for PV) from shared memory.  Measured reason: the one-tile
+// kernel takes ~2500 cycles per 64-token block against ~900 cycles of MMA time, and is neither
+// TMA nor MUFU bound (EXP_PFNOLOAD / EXP_PFNOEXP) nor softmax-latency bound (two query tiles
+// per CTA ping-ponging the tensor core: no change) — its shared memory moves ~176 KB per block
+// (TMA K/V 32, Q 32 + K 16 for S, P 32 + V 32 for PV, P stores 32) against ~128 B/clock; with Q
+// and P in TMEM it moves ~80 KB.  Q is written once per CTA (tcgen05.st, thread = row); P is
+// written by the softmax threads with tcgen05.st (32 columns of bf16 pairs per hi / lo) instead
+// of swizzled shared-memory stores.  TMEM columns (D = 128): Q [0, 64), S [64, 192) (two
+// buffers), P [192, 320) (two buffers of hi, lo), O [320, 448).
+template <int D>
+struct Pu2Cfg {
+    static constexpr int kHalves = D / 64;
+    static constexpr int kBlk = kHalves * kPuBT * 128;           // K or V block: [half][64 rows][128 B]
+    static constexpr int oK = 0;
+    static constexpr int oV = oK + kPuNB * kBlk;
+    static constexpr int oBar = oV + kPuNB * kBlk;
+    static constexpr int nBar = 4 * kPuNB + 1 + 2 * 4;
+    static constexpr int kSmem = 1024 + oBar + nBar * 8 + 16;
+    static constexpr int kTmemCols = 512;
+    static constexpr int kQCol = 0;
+    static constexpr int kSCol = 64;                              // + buffer * 64
+    static constexpr int kPCol = 192;                             // + buffer * 64: hi [0, 32), lo [32, 64)
+    static constexpr int kOCol = 320;
+};
+
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+// Issued by the whole (converged) warp: one lane, elected inside the asm, issues the MMA — no
+// divergent `if (lane == 0)` around it, so the operands can stay in uniform registers instead
+// of the per-MMA elect / broadcast loop the compiler wraps around divergent tcgen05 issue.
+__device__ __forceinline__ void umma_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kPuThreads, 1)
+prefill_umma2_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillParams p) {
+    using C = Pu2Cfg<D>;
+    extern __shared__ __align__(16) uint8_t pu_smem[];
+    uint8_t* base = pu_smem + ((1024u - (smem_u32(pu_smem) & 1023u)) & 1023u);
+    uint8_t* kring = base + C::oK;
+    uint8_t* vring = base + C::oV;
+    uint64_t* k_full = reinterpret_cast<uint64_t*>(base + C::oBar);
+    uint64_t* k_empty = k_full + kPuNB;
+    uint64_t* v_full = k_empty + kPuNB;
+    uint64_t* v_empty = v_full + kPuNB;
+    uint64_t* vz_done = v_empty + kPuNB;
+    uint64_t* s_full = vz_done + 1;
+    uint64_t* s_free = s_full + 2;
+    uint64_t* p_full = s_free + 2;
+    uint64_t* p_free = p_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_free + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int gs = p.gs, T = 128 / gs;
+    const int tile = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;  // longest rows first
+    const int t0 = tile * T;
+
+    if (tid == 0) {
+        for (int i = 0; i < kPuNB; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+        }
+        mbar_init(vz_done, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_free[i], 4);
+            mbar_init(&p_full[i], 4);
+            mbar_init(&p_free[i], 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(C::kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (warp == 4 && lane == 0) tma_prefetch_desc(&tm_kv);
+    pdl_wait();  // the chunk's append (previous kernel) wrote the pool rows and the length
+    const int s_tot = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
+    const int n0 = s_tot - p.ntok;
+    const int t_hi = min(p.ntok, t0 + T);
+    const int kv_end = n0 + t_hi;
+    const int n_pages = (kv_end + kPage - 1) / kPage;
+    const int nblk = (n_pages + kPuKB - 1) / kPuKB;
+    __syncthreads();  // the TMEM allocation is visible
+    const uint32_t tbase = *tmem_slot;
+    if (warp < 4) {  // Q row r (thread = row) into TMEM lane r, two bf16 per column
+        const int r = tid, j = r / T, i = r - j * T;
+        const bool valid = j < gs && t0 + i < p.ntok;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(reinterpret_cast<const __nv_bfloat16*>(p.q) +
+                                                                (((size_t)b * p.ntok + t0 + i) * p.m + h * gs + j) * D);
+        const uint32_t lb = tbase + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+        for (int c0 = 0; c0 < D / 2; c0 += 32) {
+            uint32_t v[32];
+#pragma unroll
+            for (int c = 0; c < 32; c += 4) {
+                const uint4 x = valid ? reinterpret_cast<const uint4*>(src + c0)[c / 4] : make_uint4(0, 0, 0, 0);
+                v[c] = x.x; v[c + 1] = x.y; v[c + 2] = x.z; v[c + 3] = x.w;
+            }
+            tmem_st32(lb + C::kQCol + c0, v);
+        }
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    pdl_launch_dependents();
+    const size_t layer_ph = (size_t)p.layer * p.num_phys;
+    const int32_t* bt = p.block_table + (size_t)b * p.bt_stride;
+    auto block_pages = [&](int i) { return min(kPuKB, n_pages - i * kPuKB); };
+    const bool tail = (kv_end % kPage) != 0;
+    if (warp == 4 || warp == 6) {
+        // ============================================================ TMA producers: K (4), V (6)
+        const bool is_v = warp == 6;
+        uint8_t* ring = is_v ? vring : kring;
+        uint64_t* fullb = is_v ? v_full : k_full;
+        uint64_t* emptyb = is_v ? v_empty : k_empty;
+        if (lane == 0) {
+            for (int i = 0; i < nblk; ++i) {
+                const int slot = i % kPuNB, round = i / kPuNB;
+                if (round > 0) mbar_wait(&emptyb[slot], (round - 1) & 1);
+                const int np = block_pages(i);
+                mbar_arrive_expect_tx(&fullb[slot], np * C::kHalves * kPage * 128);
+                for (int q = 0; q < np; ++q) {
+                    const int row0 = (int)kv_row(layer_ph + bt[i * kPuKB + q], p.g, h, 0) + (is_v ? kPage : 0);
+#pragma unroll
+                    for (int hf = 0; hf < C::kHalves; ++hf) {
+                        uint8_t* dst = ring + slot * C::kBlk + hf * (kPuBT * 128) + q * kPage * 128;
+                        if (D == 64) tma_load_2d(dst, &tm_kv, &fullb[slot], 0, row0, kEvictNormal);
+                        else tma_load_3d(dst, &tm_kv, &fullb[slot], 0, row0, hf, kEvictNormal);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (is_v && tail && nblk > 0) {  // V rows past the end in the last page: 0
+            const int i = nblk - 1, slot = i % kPuNB, q = block_pages(i) - 1, r0 = kv_end % kPage;
+            mbar_wait(&v_full[slot], (i / kPuNB) & 1);
+            uint8_t* vb = vring + slot * C::kBlk;
+            for (int ch = lane; ch < C::kHalves * (kPage - r0) * 8; ch += 32) {
+                const int hf = ch / ((kPage - r0) * 8), rem = ch - hf * (kPage - r0) * 8;
+                const int r = q * kPage + r0 + rem / 8, c = rem % 8;
+                *reinterpret_cast<uint4*>(vb + hf * (kPuBT * 128) + r * 128 + ((c ^ (r & 7)) << 4)) = make_uint4(0, 0, 0, 0);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(vz_done);
+        }
+    } else if (warp == 5) {
+        // ============================================================ MMA issuer (converged warp)
+        constexpr uint32_t kIdS = umma_idesc(128, kPuBT, 0, 0);  // A = Q (TMEM), B = K rows K-major
+        constexpr uint32_t kIdPV = umma_idesc(128, D, 0, 1);     // A = P (TMEM), B = V MN-major
+        const uint32_t tb = __shfl_sync(0xffffffffu, tbase, 0);
+        const uint64_t k_d0 = umma_desc(smem_u32(kring), 16, 1024, kLayoutSW128);
+        const uint64_t v_d0 = umma_desc(smem_u32(vring), D == 128 ? kPuBT * 128 : 0, 1024, kLayoutSW128);
+        for (int i = 0; i <= nblk; ++i) {
+            if (i < nblk) {  // S(i)
+                mbar_wait(&k_full[i % kPuNB], (i / kPuNB) & 1);
+                if (i >= 2) mbar_wait(&s_free[i & 1], ((i - 2) >> 1) & 1);
+                tc_fence_after();
+                const uint64_t kd = k_d0 + (uint64_t)(((i % kPuNB) * C::kBlk) >> 4);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    umma_ts_w(tb + C::kSCol + (i & 1) * kPuBT, tb + C::kQCol + kk * 8,
+                              kd + (uint64_t)((((kk >> 2) * (kPuBT * 128)) + (kk & 3) * 32) >> 4), kIdS, kk > 0 ? 1u : 0u);
+                umma_commit_w(&s_full[i & 1]);
+                umma_commit_w(&k_empty[i % kPuNB]);
+            }
+            if (i >= 1) {  // PV(i - 1), after its softmax wrote P
+                const int j = i - 1;
+                mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+                mbar_wait(&v_full[j % kPuNB], (j / kPuNB) & 1);
+                if (tail && j == nblk - 1) mbar_wait(vz_done, 0);
+                tc_fence_after();
+                const uint32_t pc = tb + C::kPCol + (j & 1) * 64;
+                const uint64_t vd = v_d0 + (uint64_t)(((j % kPuNB) * C::kBlk) >> 4);
+                const int np = block_pages(j);
+#pragma unroll
+                for (int q = 0; q < kPuKB; ++q) {
+                    if (q < np) {
+                        const uint64_t bv = vd + (uint64_t)((q * kPage * 128) >> 4);
+                        umma_ts_w(tb + C::kOCol, pc + q * 8, bv, kIdPV, (j > 0 || q > 0) ? 1u : 0u);
+                        umma_ts_w(tb + C::kOCol, pc + 32 + q * 8, bv, kIdPV, 1u);
+                    }
+                }
+                umma_commit_w(&v_empty[j % kPuNB]);
+                umma_commit_w(&p_free[j & 1]);
+            }
+        }
+} else if (warp < 4) {
+        // ============================================================ softmax (thread = row)
+        const int r = tid, j = r / T, i_tok = r - j * T;
+        const bool valid = j < gs && t0 + i_tok < p.ntok;
+        const int pos = n0 + t0 + i_tok;
+        const float sl2 = p.scale_log2;
+        const uint32_t lane_base = tbase + ((uint32_t)(warp * 32) << 16);
+        float m = -INFINITY, l = 0.f;
+        for (int i = 0; i < nblk; ++i) {
+            mbar_wait(&s_full[i & 1], (i >> 1) & 1);
+            tc_fence_after();
+            float x[kPuBT];
+            {
+                uint32_t v0[32], v1[32];
+                tmem_ld32(lane_base + C::kSCol + (i & 1) * kPuBT, v0);
+                tmem_ld32(lane_base + C::kSCol + (i & 1) * kPuBT + 32, v1);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    x[c] = __uint_as_float(v0[c]);
+                    x[32 + c] = __uint_as_float(v1[c]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_free[i & 1]);
+#ifdef EXP_PFNOSM
+            if (i >= 2) mbar_wait(&p_free[i & 1], ((i - 2) >> 1) & 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[i & 1]);
+            continue;
+#endif
+            float bmax = -INFINITY;
+            const int tk0 = i * kPuBT;
+#pragma unroll
+            for (int c = 0; c < kPuBT; ++c) {
+                x[c] = (valid && tk0 + c <= pos) ? x[c] * sl2 : -INFINITY;
+                bmax = fmaxf(bmax, x[c]);
+            }
+            const bool raise = bmax > m + kPuRaise || (m == -INFINITY && bmax > -INFINITY);
+            const float m_new = raise ? fmaxf(m, bmax) : m;
+            const bool rescale = raise && l > 0.f;
+            if (__any_sync(0xffffffffu, rescale)) {
+                mbar_wait(&p_free[(i - 1) & 1], ((i - 1) >> 1) & 1);
+                tc_fence_after();
+                const float al = rescale ? ex2(m - m_new) : 1.f;
+#pragma unroll
+                for (int c0 = 0; c0 < D; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(lane_base + C::kOCol + c0, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(__uint_as_float(v[c]) * al);
+                    tmem_st32(lane_base + C::kOCol + c0, v);
+                }
+                tmem_wait_st();
+                l *= al;
+            }
+            m = m_new;
+            const float msafe = m == -INFINITY ? 0.f : m;
+            if (i >= 2) mbar_wait(&p_free[i & 1], ((i - 2) >> 1) & 1);  // PV(i - 2) done with this P buffer
+            tc_fence_after();
+            uint32_t hw[32], lw[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const float p0 = ex2(x[2 * c] - msafe), p1 = ex2(x[2 * c + 1] - msafe);
+                l += p0 + p1;
+                const __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
+                const float2 hf = __bfloat1622float2(hv);
+                hw[c] = *reinterpret_cast<const uint32_t*>(&hv);
+                lw[c] = pack_bf16(p0 - hf.x, p1 - hf.y);
+            }
+            tmem_st32(lane_base + C::kPCol + (i & 1) * 64, hw);
+            tmem_st32(lane_base + C::kPCol + (i & 1) * 64 + 32, lw);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[i & 1]);
+        }
+        // ------------------------------------------------------------ epilogue: O / l
+        if (nblk > 0) mbar_wait(&p_free[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);  // the last PV completed
+        tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        float* dst = p.out + (((size_t)b * p.ntok + t0 + i_tok) * p.m + h * gs + j) * D;
+        bool bad = false;
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(lane_base + C::kOCol + c0, v);
+            tmem_wait_ld();
+            if (valid) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    const float4 o = make_float4(__uint_as_float(v[c]) * inv, __uint_as_float(v[c + 1]) * inv,
+                                                 __uint_as_float(v[c + 2]) * inv, __uint_as_float(v[c + 3]) * inv);
+                    bad |= !(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w));
+                    *reinterpret_cast<float4*>(dst + c0 + c) = o;
+                }
+            }
+        }
+        if (valid && p.lse_out)
+            p.lse_out[((size_t)b * p.ntok + t0 + i_tok) * p.m + h * gs + j] =
+                l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
+        if (bad) set_err(p.err, kDevNumeric);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::kTmemCols));
+}
+
 }  // namespace
 
 bool prefill_umma_supported(const PrefillParams& p) { return (p.d == 128 || p.d == 64) && p.gs <= 16; }
+
+cudaError_t launch_prefill_umma2(const PrefillParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl) {
+    const void* fn = p.d == 128 ? (const void*)prefill_umma2_kernel<128> : (const void*)prefill_umma2_kernel<64>;
+    const int smem = p.d == 128 ? Pu2Cfg<128>::kSmem : Pu2Cfg<64>::kSmem;
+    static std::atomic<int> cache[kMaxDevices * 2];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+    const int slot = dev * 2 + (p.d == 128 ? 0 : 1);
+    if (cache[slot].load(std::memory_order_acquire) == 0) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        cache[slot].store(1, std::memory_order_release);
+    }
+    const int T = 128 / p.gs;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((p.ntok + T - 1) / T, p.g, p.batch);
+    cfg.blockDim = dim3(kPuThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    void* args[] = {const_cast<CUtensorMap*>(tm_kv), const_cast<PrefillParams*>(&p)};
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
 
 cudaError_t launch_prefill_umma(const PrefillParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl) {
     const void* fn = p.d == 128 ? (const void*)prefill_umma_kernel<128> : (const void*)prefill_umma_kernel<64>;
