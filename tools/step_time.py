@@ -22,23 +22,26 @@ def main():
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--ctx", type=int, default=32768)
+    ap.add_argument("--config", default="c1", choices=["c1", "c4"])
     a = ap.parse_args()
     ctx = a.ctx
-    L, m, g, d, F, delta = 32, 32, 8, 128, 2, [2, 16, 25]
-    mk = lambda sel: d200.DeltaConfig(num_layers=L, num_q_heads=m, num_kv_heads=g, head_dim=d, max_batch=1,
+    L, m, g, d, F, delta, B = 32, 32, 8, 128, 2, [2, 16, 25], 1
+    if a.config == "c4":  # Qwen3-14B shape, 8 sequences (bench.py c4)
+        L, m, g, d, F, delta, B = 40, 40, 8, 128, 2, [2, 6, 35], 8
+    mk = lambda sel: d200.DeltaConfig(num_layers=L, num_q_heads=m, num_kv_heads=g, head_dim=d, max_batch=B,
                                       max_seq_len=ctx + a.steps + 64, num_full_prefix=F if sel else L,
                                       select_layers=delta if sel else [], budget_k=2048, n_sink=4, n_window=32,
                                       select_block=16)
     cfg = mk(True)
-    bt = torch.from_numpy(synth.block_table(7, 1, cfg.max_pages))
+    bt = torch.from_numpy(synth.block_table(7, B, cfg.max_pages))
     base = d200.DeltaStack.allocate(cfg, bt)
-    sd.fill_pools(base.kv_pool, base.block_table, 7, ctx - 1, 1, range(L))
-    q = torch.empty((L, 1, m, d), dtype=torch.bfloat16, device="cuda")
-    k = torch.empty((L, 1, g, d), dtype=torch.bfloat16, device="cuda")
+    sd.fill_pools(base.kv_pool, base.block_table, 7, ctx - 1, B, range(L))
+    q = torch.empty((L, B, m, d), dtype=torch.bfloat16, device="cuda")
+    k = torch.empty((L, B, g, d), dtype=torch.bfloat16, device="cuda")
     v = torch.empty_like(k)
-    sd.fill_queries(q, 7, range(L), [ctx])
-    sd.fill_new_kv(k, v, 7, range(L), [ctx - 1])
-    out = torch.empty((L, 1, m, d), dtype=torch.float32, device="cuda")
+    sd.fill_queries(q, 7, range(L), [ctx] * B)
+    sd.fill_new_kv(k, v, 7, range(L), [ctx - 1] * B)
+    out = torch.empty((L, B, m, d), dtype=torch.float32, device="cuda")
     s = torch.cuda.Stream()
     for tune in os.environ.get("PROBE_TUNES", "auto").split(";"):
         if tune == "auto":
@@ -50,7 +53,7 @@ def main():
             c = mk(sel)
             _, ws = d200.query_sizes(c)
             st = d200.DeltaStack(c, base.kv_pool, base.block_table, torch.zeros(ws, dtype=torch.uint8, device="cuda"))
-            st.set_seq_lens([ctx - 1])
+            st.set_seq_lens([ctx - 1] * B)
             with torch.cuda.stream(s):
                 for _ in range(5):
                     st.decode_step(q, k, v, out, stream=s)
@@ -69,10 +72,10 @@ def main():
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 with torch.cuda.stream(s):
                     for _ in range(5):
-                        st.select(delta[0], 1, stream=s)
+                        st.select(delta[0], B, stream=s)
                     e0.record(s)
                     for _ in range(50):
-                        st.select(delta[0], 1, stream=s)
+                        st.select(delta[0], B, stream=s)
                     e1.record(s)
                 s.synchronize()
                 print(f"   [{tune}] eager select {1e3 * e0.elapsed_time(e1) / 50:.2f} us", flush=True)
