@@ -515,3 +515,37 @@ def test_injected_nan_sets_sticky_numeric_error(where):
     st.synchronize()
     assert case.stack.get_error(stream=st) == 0
     assert not torch.isnan(out).any()
+
+
+def test_gmerge_ll_flags_across_split_counts_and_protocols():
+    """The global split-K merge's LL flags carry the split count and a per-(b, h, split count)
+    launch epoch (combine.cuh): launches with different split counts, and the ticket protocol
+    (gll = 0) interleaved with LL launches, reuse the same partial slots — a flag that aliased
+    across them would let a merge accept another launch's partials.  Each step checks every
+    layer against the oracle."""
+    sh = Shape(L=2, m=32, g=8, d=128, F=2, delta=[], k=0, S=0, Lw=0, block=16, dtype="bf16")
+    case = GpuCase(sh, 41, batch=1, s_pre=3000, max_seq=3100)
+    s = 3000
+    for tune in [("nsplit", 18), ("nsplit", 12), ("nsplit", 18), ("gll", 0), ("gll", 1), ("nsplit", 7),
+                 ("nsplit", 12)]:
+        case.stack.set_tuning(*tune)
+        s += 1
+        out, lse, plans = case.step_layers(s)
+        _check_step(case, s, out, lse, plans)
+
+
+def test_select_ll_keys_do_not_alias_across_delta_layers():
+    """Three Delta layers share the select's LL key buffer; their epochs must never coincide
+    (one epoch per sequence, not per layer): several steps through the per-layer ABI and the
+    captured step, plans checked against the oracle's."""
+    sh = Shape(L=6, m=32, g=8, d=128, F=1, delta=[1, 3, 4], k=256, S=4, Lw=32, block=16, dtype="bf16")
+    case = GpuCase(sh, 43, batch=2, s_pre=6000, max_seq=6100)
+    for s in (6001, 6002, 6003):
+        out, lse, plans = case.step_layers(s)
+        _check_step(case, s, out, lse, plans)
+    for s in (6004, 6005):
+        out, lse = case.step_graph(s)
+        ref = [oracle_step(sh, case.seed, b, s) for b in range(case.batch)]
+        for b in range(case.batch):
+            for l in range(sh.L):
+                assert_close_bf16(out[l, b], ref[b][l][0], f"graph step s={s} layer {l} seq {b}")
