@@ -116,6 +116,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     if (tid == 0) DTRACE(1);
 
     // ---------------------------------------------------------------- geometry
+    // fixed_part: the producer's first block-table entries do not depend on the length, so they
+    // are loaded in the same round trip as the length counter (used if the geometry agrees)
+    int spec_phys = 0;
+    const int spec_u0 = max(0, p.page_lo) +
+                        split * ((max(0, min(p.bt_stride, p.page_hi) - max(0, p.page_lo)) + p.nsplit - 1) / p.nsplit);
+    if (!TOKEN_PLAN && p.fixed_part && p.role != kRoleSparse && warp == NCW && lane < kBatch &&
+        spec_u0 + lane < p.bt_stride)
+        spec_phys = p.block_table[(size_t)b * p.bt_stride + spec_u0 + lane];
     const int n_old = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
     const int s = p.fuse_append ? n_old + 1 : n_old;
     const bool cap_err = s > p.max_seq;
@@ -184,7 +192,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
                 }
             };
             int my_lp, my_phys;
-            resolve(0, my_lp, my_phys);
+            if (p.fixed_part && p.role != kRoleSparse && unit0 == spec_u0) {  // the speculative entries
+                my_lp = (lane < kBatch && lane < n_items) ? unit0 + lane : -1;
+                my_phys = my_lp >= 0 ? spec_phys : 0;
+            } else {
+                resolve(0, my_lp, my_phys);
+            }
             for (int base = 0; base < n_items; base += kBatch) {
                 if (base > 0) resolve(base, my_lp, my_phys);
                 const int nb = min(kBatch, n_items - base);

@@ -121,8 +121,17 @@ __device__ __forceinline__ void split_geometry(const AttnParams& p, int b, int s
     if (p.role != kRoleSparse) {
         const int npages = (s + kPage - 1) / kPage;
         const int lo = max(0, p.page_lo), hi = min(npages, p.page_hi), n = max(0, hi - lo);
-        unit0 = lo + (int)((long long)split * n / p.nsplit);
-        n_items = lo + (int)((long long)(split + 1) * n / p.nsplit) - unit0;
+        const int maxr = max(0, min(p.bt_stride, p.page_hi) - lo), pf = (maxr + p.nsplit - 1) / p.nsplit;
+        if (p.fixed_part && n * 16 >= maxr * 15) {
+            // fixed_part: split c starts at page c * ceil(max / nsplit) whatever s is (while the
+            // cache is at least 15/16 full), so a producer can load its first block-table entries
+            // together with the length counter instead of after it (attn_tc.cu)
+            unit0 = lo + min(n, split * pf);
+            n_items = lo + min(n, (split + 1) * pf) - unit0;
+        } else {
+            unit0 = lo + (int)((long long)split * n / p.nsplit);
+            n_items = lo + (int)((long long)(split + 1) * n / p.nsplit) - unit0;
+        }
     } else {
         stale = p.plan_stamp[b] != s;
         const int cnt = stale ? 0 : p.plan_count[b];

@@ -363,7 +363,7 @@ struct delta_ctx {
     // cycles to issue (tools/umma_test.cu), so 10 per tile lose to the mma.sync kernel here;
     // kept selectable (DELTA_TUNE umma=1) and parity-tested.
     int tune_prewait = 1, tune_early = 1, tune_umma = 0, tune_policy = 0;
-    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1, tune_gm2 = 0, tune_lat = 1, tune_qpf = 1, tune_pfumma = 2, tune_gll = 1, tune_selll = 1;
+    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1, tune_gm2 = 0, tune_lat = 1, tune_qpf = 1, tune_pfumma = 2, tune_gll = 1, tune_selll = 1, tune_gfix = 1;
     // sequence sharding
     int world = 1, rank = 0, page_lo = 0, page_hi = 0x7fffffff;
     ncclComm_t comm = nullptr;  // null with world > 1: the caller exchanges (delta_shard_* calls)
@@ -448,6 +448,7 @@ AttnParams attn_params(delta_ctx* h, int layer, int batch, int role_override = -
         p.gcnt = h->at<unsigned long long>(h->L.gcnt);
         p.gm_shallow = h->tune_gm2;
         p.gll = h->tune_gll;
+        p.fixed_part = (p.role != kRoleSparse && h->world == 1 && !h->L.det_chunks) ? h->tune_gfix : 0;
     }
     const int cap = p.gmerge ? std::min(kMaxSplitG, h->L.gslots / std::max(1, batch * c.num_kv_heads)) : kMaxSplit;
     if (h->tune_nsplit > 0) p.nsplit = std::min(h->tune_nsplit, cap);
@@ -1343,7 +1344,7 @@ delta_status delta_set_tuning(delta_t h, const char* key, int32_t value) {
         {"nsplit", &h->tune_nsplit}, {"snsplit", &h->tune_snsplit}, {"deep", &h->tune_deep},
         {"prewait", &h->tune_prewait}, {"early", &h->tune_early}, {"umma", &h->tune_umma},
         {"policy", &h->tune_policy}, {"seltrig", &h->tune_seltrig}, {"selhist", &h->tune_selhist},
-        {"gmerge", &h->tune_gmerge}, {"gm2", &h->tune_gm2}, {"lat", &h->tune_lat}, {"qpf", &h->tune_qpf}, {"pfumma", &h->tune_pfumma}, {"gll", &h->tune_gll}, {"selll", &h->tune_selll}};
+        {"gmerge", &h->tune_gmerge}, {"gm2", &h->tune_gm2}, {"lat", &h->tune_lat}, {"qpf", &h->tune_qpf}, {"pfumma", &h->tune_pfumma}, {"gll", &h->tune_gll}, {"selll", &h->tune_selll}, {"gfix", &h->tune_gfix}};
     for (const Knob& k : knobs)
         if (std::strcmp(k.name, key) == 0) {
             *k.field = value;

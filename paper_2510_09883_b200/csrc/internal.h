@@ -67,6 +67,7 @@ struct AttnParams {
     int sparse_lat;     // host: SPARSE layer takes the latency kernel (attn_sparse.cu)
     int gm_shallow;     // gmerge: 1 = shallow ring (two CTAs per SM: the next layer's CTAs co-reside
                         //    and prefetch during this one), 0 = deep ring (one CTA per SM)
+    int fixed_part;     // FULL / SELECT: fixed page partition when the cache is >= 15/16 full (split_geometry)
     int gll;            // gmerge: 1 = partials as LL (value, flag) words polled by the merging CTAs
     float* gpart;       // gmerge: [batch][g][nsplit][gpart_floats(d)] split partials (x2 words with gll)
     unsigned long long* gcnt;  // gmerge: [max_batch][g][kMaxSplitG] ticket counters, by split count
