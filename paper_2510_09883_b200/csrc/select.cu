@@ -185,6 +185,15 @@ __device__ __forceinline__ int topk_regs(const SelectParams& p, int n_units, int
     uint32_t* s_key = sm_keys;                                                  // [n_units]
     int32_t* s_phys = reinterpret_cast<int32_t*>(sm_keys + n_units);            // [n_units]
     bool bad = false;
+    // the units' physical locations first: independent loads in flight before the key polls (a
+    // block-table load after each poll — asm volatile with a memory clobber — would serialise:
+    // one L2 round trip per unit per thread, ~7 us at 16 units per thread)
+    int32_t ph[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        const int u = i * kSelThreads + tid;
+        ph[i] = u < n_units ? phys_of(u) : 0;
+    }
     uint2 w[IPT];  // LL: one round of independent loads, then re-poll the words not yet published
     if (kll) {
 #pragma unroll
@@ -205,7 +214,7 @@ __device__ __forceinline__ int topk_regs(const SelectParams& p, int n_units, int
                 f = __ldcg(src + u);
             }
             s_key[u] = key_bits(f);
-            s_phys[u] = phys_of(u);
+            s_phys[u] = ph[i];
             bad |= isnan(f);
         }
     }

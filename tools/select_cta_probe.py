@@ -25,7 +25,7 @@ def rd():
     return buf.reshape(64, 512, 12).astype(np.int64).copy()
 
 
-ctx, L, m, g, d = 32768, 32, 32, 8, 128
+ctx, L, m, g, d = int(os.environ.get('PROBE_CTX', '32768')), 32, 32, 8, 128
 cfg = d200.DeltaConfig(num_layers=L, num_q_heads=m, num_kv_heads=g, head_dim=d, max_batch=1, max_seq_len=ctx + 64,
                        num_full_prefix=2, select_layers=[2, 16, 25], budget_k=2048, n_sink=4, n_window=32,
                        select_block=16)
