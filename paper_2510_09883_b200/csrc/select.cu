@@ -188,44 +188,59 @@ __device__ __forceinline__ int topk_regs(const SelectParams& p, int n_units, int
     // the units' physical locations first: independent loads in flight before the key polls (a
     // block-table load after each poll — asm volatile with a memory clobber — would serialise:
     // one L2 round trip per unit per thread, ~7 us at 16 units per thread)
-    int32_t ph[IPT];
+    // (in groups of at most 8 units, so the in-flight words stay in registers: 64 per thread)
+    constexpr int GS = IPT < 8 ? IPT : 8;
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        const int u = i * kSelThreads + tid;
-        ph[i] = u < n_units ? phys_of(u) : 0;
-    }
-    uint2 w[IPT];  // LL: one round of independent loads, then re-poll the words not yet published
-    if (kll) {
+    for (int g0 = 0; g0 < IPT; g0 += GS) {
+        int32_t ph[GS];
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            const int u = i * kSelThreads + tid;
-            if (u < n_units) w[i] = ld_key_ll(kll + u);
+        for (int i = 0; i < GS; ++i) {
+            const int u = (g0 + i) * kSelThreads + tid;
+            ph[i] = u < n_units ? phys_of(u) : 0;
         }
-    }
+        uint2 w[GS];  // LL: one round of independent loads, then re-poll the words not yet published
+        if (kll) {
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        const int u = i * kSelThreads + tid;
-        if (u < n_units) {
-            float f;
-            if (kll) {
-                while (w[i].y != llf) w[i] = ld_key_ll(kll + u);
-                f = __uint_as_float(w[i].x);
-            } else {
-                f = __ldcg(src + u);
+            for (int i = 0; i < GS; ++i) {
+                const int u = (g0 + i) * kSelThreads + tid;
+                if (u < n_units) w[i] = ld_key_ll(kll + u);
             }
-            s_key[u] = key_bits(f);
-            s_phys[u] = ph[i];
-            bad |= isnan(f);
+        }
+#pragma unroll
+        for (int i = 0; i < GS; ++i) {
+            const int u = (g0 + i) * kSelThreads + tid;
+            if (u < n_units) {
+                float f;
+                if (kll) {
+                    while (w[i].y != llf) w[i] = ld_key_ll(kll + u);
+                    f = __uint_as_float(w[i].x);
+                } else {
+                    f = __ldcg(src + u);
+                }
+                s_key[u] = key_bits(f);
+                s_phys[u] = ph[i];
+                bad |= isnan(f);
+            }
         }
     }
     __syncthreads();
     if (tid == 0) DTRACE(11);
     uint32_t cand = 0, live = 0;
+    if (u0 + IPT <= n_units) {  // 16-byte loads: scalar ones at a stride of IPT words conflict IPT-way
+#pragma unroll
+        for (int j = 0; j < IPT / 4; ++j) {
+            const uint4 x = reinterpret_cast<const uint4*>(s_key + u0)[j];
+            key[4 * j] = x.x; key[4 * j + 1] = x.y; key[4 * j + 2] = x.z; key[4 * j + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) key[i] = u0 + i < n_units ? s_key[u0 + i] : 0u;
+    }
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
         const int u = u0 + i;
         const bool in = i < ipt && u < n_units;
-        key[i] = in ? s_key[u] : 0u;
+        if (!in) key[i] = 0u;
         if (in) live |= 1u << i;
         if (in && !forced(u)) cand |= 1u << i;
     }
