@@ -112,6 +112,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     // stream start before the wait — the cache rows < s-1, the block table and the plan are
     // then at least two kernels old, hence complete — and only the consumers (q, k_new, v_new,
     // outputs) wait, so the first stages land while the previous layer finishes.
+    // the consumers' q rows (read right after the wait): warm L2 and the translation before it
+    if (p.q_prefetch && warp == 0 && lane < (p.gs * D * 2 + 127) / 128) {
+        const char* qrow = reinterpret_cast<const char*>(p.q) + ((size_t)b * p.m + h * p.gs) * D * 2;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow + lane * 128));
+    }
     if (!p.prewait) pdl_wait();
     if (tid == 0) DTRACE(1);
 

@@ -377,6 +377,18 @@ __global__ void __launch_bounds__(kSelThreads, 1024 / kSelThreads) select_kernel
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int b = blockIdx.y;
     if (tid == 0) DTRACE(0);
+    // warm the address translation (and L2) of the words read right after the wait: a prefetch
+    // reads nothing, so it may precede griddepcontrol.wait
+    if (tid < 8) {
+        const char* a = nullptr;
+        if (tid == 0) a = reinterpret_cast<const char*>(p.seq_len + p.layer * p.max_batch + b);
+        if (tid == 1) a = reinterpret_cast<const char*>(p.lse_buf + (size_t)b * p.m);
+        if (tid == 2 && p.ll) a = reinterpret_cast<const char*>(p.epoch + b);
+        if (tid == 3 && p.ll) a = reinterpret_cast<const char*>(p.keys_ll + (size_t)b * p.max_units);
+        if (tid >= 4) a = reinterpret_cast<const char*>(p.logits + ((size_t)b * p.max_seq +
+                          (size_t)(tid - 4) * (p.max_seq / 4) + (size_t)blockIdx.x * p.max_seq / (4 * gridDim.x)) * p.m);
+        if (a && !p.keys_override && !p.k_new) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
     pdl_wait();
     if (!p.late_trigger) pdl_launch_dependents();  // the next kernel's reads of this plan come after its own wait
     if (tid == 0) DTRACE(1);
