@@ -9,11 +9,13 @@ run() {  # tool, test spec
 }
 for t in "tests/test_gpu_parity.py -k gs16" "tests/test_gpu_parity.py -k c0_page" "tests/test_gpu_raas.py -k 1" \
          "tests/test_gpu_quest.py -k d64" "tests/test_gpu_recall.py -k quest" "tests/test_gpu_prefill.py -k d64" \
-         "tests/test_gpu_shard.py -k det_chunks_bitwise" "tests/test_gpu_parity.py -k heads_ragged"; do
+         "tests/test_gpu_shard.py -k det_chunks_bitwise" "tests/test_gpu_parity.py -k heads_ragged" \
+         "tests/test_gpu_parity.py -k ll_flags" "tests/test_gpu_parity.py -k ll_keys" "tests/test_gpu_prefill.py"; do
   run racecheck "$t"
 done
 for t in "tests/test_gpu_parity.py -k c0_page" "tests/test_gpu_shard.py -k det_chunks" "tests/test_gpu_raas.py -k 1" \
-         "tests/test_gpu_prefill.py" "tests/test_gpu_quest.py -k d64"; do
+         "tests/test_gpu_prefill.py" "tests/test_gpu_quest.py -k d64" "tests/test_gpu_parity.py -k ll_flags" \
+         "tests/test_gpu_parity.py -k ll_keys" "tests/test_gpu_parity.py -k heads_ragged"; do
   run memcheck "$t"
 done
 cat $out
