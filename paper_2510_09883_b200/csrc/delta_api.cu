@@ -363,7 +363,7 @@ struct delta_ctx {
     // cycles to issue (tools/umma_test.cu), so 10 per tile lose to the mma.sync kernel here;
     // kept selectable (DELTA_TUNE umma=1) and parity-tested.
     int tune_prewait = 1, tune_early = 1, tune_umma = 0, tune_policy = 0;
-    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1, tune_gm2 = 0, tune_lat = 1, tune_qpf = 1, tune_pfumma = 2, tune_gll = 1, tune_selll = 1, tune_gfix = 1;
+    int tune_seltrig = 0, tune_selhist = 0, tune_gmerge = 1, tune_gm2 = 0, tune_lat = 1, tune_qpf = 1, tune_pfumma = 3, tune_gll = 1, tune_selll = 1, tune_gfix = 1;
     // sequence sharding
     int world = 1, rank = 0, page_lo = 0, page_hi = 0x7fffffff;
     ncclComm_t comm = nullptr;  // null with world > 1: the caller exchanges (delta_shard_* calls)
@@ -1232,7 +1232,8 @@ delta_status delta_prefill(delta_t h, int32_t layer, int32_t batch, int32_t ntok
     p.q = q; p.kv_pool = h->kv_pool; p.block_table = h->block_table; p.seq_len = h->at<int32_t>(h->L.seq_len);
     p.out = out; p.lse_out = lse_out; p.err = h->at<int32_t>(h->L.err);
     // tcgen05 / TMEM kernel (prefill_umma.cu); the mma.sync kernel stays selectable (pfumma=0)
-    cudaError_t e = (h->tune_pfumma == 2 && prefill_umma_supported(p)) ? launch_prefill_umma2(p, &h->tm_kvp, stream, h->pdl)
+    cudaError_t e = (h->tune_pfumma == 3 && prefill_umma_supported(p)) ? launch_prefill_umma3(p, &h->tm_kvp, stream, h->pdl)
+                    : (h->tune_pfumma == 2 && prefill_umma_supported(p)) ? launch_prefill_umma2(p, &h->tm_kvp, stream, h->pdl)
                     : (h->tune_pfumma && prefill_umma_supported(p)) ? launch_prefill_umma(p, &h->tm_kvp, stream, h->pdl)
                                                                       : launch_prefill(p, stream, h->pdl);
     if (e != cudaSuccess) return cuda_fail(h, e, "prefill launch");

@@ -211,6 +211,7 @@ struct PrefillParams {
 cudaError_t launch_prefill(const PrefillParams& p, cudaStream_t st, bool pdl);
 cudaError_t launch_prefill_umma(const PrefillParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl);
 cudaError_t launch_prefill_umma2(const PrefillParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl);
+cudaError_t launch_prefill_umma3(const PrefillParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl);
 bool prefill_umma_supported(const PrefillParams& p);
 size_t prefill_smem_bytes(int d, int gs);
 

@@ -655,6 +655,322 @@ prefill_umma2_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPar
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::kTmemCols));
 }
 
+// ================================================================================================
+// Two query tiles per CTA on the converged-issue pipeline (pfumma = 3): tiles A = 2c and B = 2c + 1
+// of one (kv head, sequence) share every K / V block and alternate on the tensor core — S_A(i),
+// S_B(i), then PV_A(i - 1), PV_B(i - 1) — so one tile's softmax runs while the other tile's MMAs
+// execute.  TMEM budget (512 columns): per tile one S buffer (64 columns), one P buffer (hi
+// [0, 32), lo [32, 64)) and O — single-buffered per tile, the other tile fills the gaps; Q of both
+// tiles in shared memory.  (Writing P over its own S, two S/P buffers per tile, measured faster but
+// wrong: an MMA writing S over the columns the previous PV still reads is not ordered for us.)
+constexpr int kPu3Threads = 352;  // softmax of A: warps 0-3, of B: 4-7; K producer 8, MMA 9, V producer 10
+
+template <int D>
+struct Pu3Cfg {
+    static constexpr int kHalves = D / 64;
+    static constexpr int kQ = kHalves * 128 * 128;               // one tile's Q: [half][128 rows][128 B]
+    static constexpr int kBlk = kHalves * kPuBT * 128;
+    static constexpr int oQ = 0;
+    static constexpr int oK = oQ + 2 * kQ;
+    static constexpr int oV = oK + kPuNB * kBlk;
+    static constexpr int oBar = oV + kPuNB * kBlk;
+    static constexpr int nBar = 4 * kPuNB + 1 + 4 * 2;
+    static constexpr int kSmem = 1024 + oBar + nBar * 8 + 16;
+    static constexpr int kTmemCols = 512;
+    static constexpr int kTile = 256;                            // TMEM columns per tile: S, P at +64, O at +128
+};
+
+__device__ __forceinline__ void umma_ss_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+template <int D>
+__global__ void __launch_bounds__(kPu3Threads, 1)
+prefill_umma3_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillParams p) {
+    using C = Pu3Cfg<D>;
+    extern __shared__ __align__(16) uint8_t pu_smem[];
+    uint8_t* base = pu_smem + ((1024u - (smem_u32(pu_smem) & 1023u)) & 1023u);
+    uint8_t* kring = base + C::oK;
+    uint8_t* vring = base + C::oV;
+    uint64_t* k_full = reinterpret_cast<uint64_t*>(base + C::oBar);
+    uint64_t* k_empty = k_full + kPuNB;
+    uint64_t* v_full = k_empty + kPuNB;
+    uint64_t* v_empty = v_full + kPuNB;
+    uint64_t* vz_done = v_empty + kPuNB;
+    uint64_t* s_full = vz_done + 1;   // [tile]: one phase per block
+    uint64_t* s_free = s_full + 2;    // [tile]: the softmax read S
+    uint64_t* p_full = s_free + 2;    // [tile]: the softmax wrote P
+    uint64_t* p_free = p_full + 2;    // [tile]: PV completed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_free + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int gs = p.gs, T = 128 / gs;
+    const int ntiles = (p.ntok + T - 1) / T;
+    const int pair = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;  // longest rows first
+    const bool hasB = 2 * pair + 1 < ntiles;
+
+    if (tid == 0) {
+        for (int i = 0; i < kPuNB; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+        }
+        mbar_init(vz_done, 1);
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(&s_full[x], 1);
+            mbar_init(&s_free[x], 4);
+            mbar_init(&p_full[x], 4);
+            mbar_init(&p_free[x], 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(C::kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (warp == 8 && lane == 0) tma_prefetch_desc(&tm_kv);
+    pdl_wait();  // the chunk's append (previous kernel) wrote the pool rows and the length
+    const int s_tot = p.seq_len[p.layer * p.max_batch + b] / p.g;  // raw counter = n * g
+    const int n0 = s_tot - p.ntok;
+    auto tile_blocks = [&](int x) {
+        const int kv_end = n0 + min(p.ntok, (2 * pair + x) * T + T);
+        return ((kv_end + kPage - 1) / kPage + kPuKB - 1) / kPuKB;
+    };
+    const int nblkA = tile_blocks(0);
+    const int nblk = hasB ? tile_blocks(1) : nblkA;
+    const int kv_end = n0 + min(p.ntok, (2 * pair + (hasB ? 1 : 0)) * T + T);
+    const int n_pages = (kv_end + kPage - 1) / kPage;
+    if (warp < 8) {  // Q rows of tile warp / 4 (thread = row), K-major SW128
+        const int x = warp >> 2, r = tid & 127, j = r / T, i = r - j * T;
+        const int t0 = (2 * pair + x) * T;
+        const bool valid = (x == 0 || hasB) && j < gs && t0 + i < p.ntok;
+        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.q) +
+                                                          (((size_t)b * p.ntok + t0 + i) * p.m + h * gs + j) * D);
+        uint8_t* qs = base + C::oQ + x * C::kQ;
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) {
+            const uint4 v = valid ? src[c] : make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(qs + (c >> 3) * 16384 + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+        }
+        fence_proxy_async_smem();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    pdl_launch_dependents();
+    const uint32_t tbase = *tmem_slot;
+    const size_t layer_ph = (size_t)p.layer * p.num_phys;
+    const int32_t* bt = p.block_table + (size_t)b * p.bt_stride;
+    auto block_pages = [&](int i) { return min(kPuKB, n_pages - i * kPuKB); };
+    const bool tail = (kv_end % kPage) != 0;
+
+    if (warp == 8 || warp == 10) {
+        // ============================================================ TMA producers (K: 8, V: 10)
+        const bool is_v = warp == 10;
+        uint8_t* ring = is_v ? vring : kring;
+        uint64_t* fullb = is_v ? v_full : k_full;
+        uint64_t* emptyb = is_v ? v_empty : k_empty;
+        if (lane == 0) {
+            for (int i = 0; i < nblk; ++i) {
+                const int slot = i % kPuNB, round = i / kPuNB;
+                if (round > 0) mbar_wait(&emptyb[slot], (round - 1) & 1);
+                const int np = block_pages(i);
+                mbar_arrive_expect_tx(&fullb[slot], np * C::kHalves * kPage * 128);
+                for (int q = 0; q < np; ++q) {
+                    const int row0 = (int)kv_row(layer_ph + bt[i * kPuKB + q], p.g, h, 0) + (is_v ? kPage : 0);
+#pragma unroll
+                    for (int hf = 0; hf < C::kHalves; ++hf) {
+                        uint8_t* dst = ring + slot * C::kBlk + hf * (kPuBT * 128) + q * kPage * 128;
+                        if (D == 64) tma_load_2d(dst, &tm_kv, &fullb[slot], 0, row0, kEvictNormal);
+                        else tma_load_3d(dst, &tm_kv, &fullb[slot], 0, row0, hf, kEvictNormal);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (is_v && tail && nblk > 0) {  // V rows past the end of the last page: 0
+            const int i = nblk - 1, slot = i % kPuNB, q = block_pages(i) - 1, r0 = kv_end % kPage;
+            mbar_wait(&v_full[slot], (i / kPuNB) & 1);
+            uint8_t* vb = vring + slot * C::kBlk;
+            for (int ch = lane; ch < C::kHalves * (kPage - r0) * 8; ch += 32) {
+                const int hf = ch / ((kPage - r0) * 8), rem = ch - hf * (kPage - r0) * 8;
+                const int r = q * kPage + r0 + rem / 8, c = rem % 8;
+                *reinterpret_cast<uint4*>(vb + hf * (kPuBT * 128) + r * 128 + ((c ^ (r & 7)) << 4)) = make_uint4(0, 0, 0, 0);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(vz_done);
+        }
+    } else if (warp == 9) {
+        // ============================================================ MMA issuer (converged warp)
+        constexpr uint32_t kIdS = umma_idesc(128, kPuBT, 0, 0);  // A = Q (smem), B = K rows K-major
+        constexpr uint32_t kIdPV = umma_idesc(128, D, 0, 1);     // A = P (TMEM), B = V MN-major
+        const uint32_t tb = __shfl_sync(0xffffffffu, tbase, 0);
+        const uint64_t k_d0 = umma_desc(smem_u32(kring), 16, 1024, kLayoutSW128);
+        const uint64_t v_d0 = umma_desc(smem_u32(vring), D == 128 ? kPuBT * 128 : 0, 1024, kLayoutSW128);
+        const uint64_t q_d0 = umma_desc(smem_u32(base + C::oQ), 16, 1024, kLayoutSW128);
+        for (int i = 0; i <= nblk; ++i) {
+            if (i < nblk) {  // S_A(i), S_B(i)
+                mbar_wait(&k_full[i % kPuNB], (i / kPuNB) & 1);
+                tc_fence_after();
+                const uint64_t kd = k_d0 + (uint64_t)(((i % kPuNB) * C::kBlk) >> 4);
+#pragma unroll
+                for (int x = 0; x < 2; ++x) {
+                    if (x == 0 ? i >= nblkA : !hasB) continue;
+                    if (i >= 1) {
+                        mbar_wait(&s_free[x], (i - 1) & 1);  // softmax_X(i - 1) read S
+                        tc_fence_after();
+                    }
+                    const uint64_t qd = q_d0 + (uint64_t)((x * C::kQ) >> 4);
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t off = (uint32_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+                        const uint32_t offk = (uint32_t)((((kk >> 2) * (kPuBT * 128)) + (kk & 3) * 32) >> 4);
+                        umma_ss_w(tb + x * C::kTile, qd + off, kd + offk, kIdS, kk > 0 ? 1u : 0u);
+                    }
+                    umma_commit_w(&s_full[x]);
+                }
+                umma_commit_w(&k_empty[i % kPuNB]);
+            }
+            if (i >= 1) {  // PV_A(i - 1), PV_B(i - 1), each after its softmax wrote P over its S
+                const int j = i - 1;
+                mbar_wait(&v_full[j % kPuNB], (j / kPuNB) & 1);
+                if (tail && j == nblk - 1) mbar_wait(vz_done, 0);
+                const uint64_t vd = v_d0 + (uint64_t)(((j % kPuNB) * C::kBlk) >> 4);
+                const int np = block_pages(j);
+#pragma unroll
+                for (int x = 0; x < 2; ++x) {
+                    if (x == 0 ? j >= nblkA : !hasB) continue;
+                    mbar_wait(&p_full[x], j & 1);
+                    tc_fence_after();
+                    const uint32_t pc = tb + x * C::kTile + 64;
+#pragma unroll
+                    for (int q = 0; q < kPuKB; ++q) {
+                        if (q < np) {
+                            const uint64_t bv = vd + (uint64_t)((q * kPage * 128) >> 4);
+                            umma_ts_w(tb + x * C::kTile + 128, pc + q * 8, bv, kIdPV, (j > 0 || q > 0) ? 1u : 0u);
+                            umma_ts_w(tb + x * C::kTile + 128, pc + 32 + q * 8, bv, kIdPV, 1u);
+                        }
+                    }
+                    umma_commit_w(&p_free[x]);
+                }
+                umma_commit_w(&v_empty[j % kPuNB]);
+            }
+        }
+    } else if (warp < 8) {
+        // ============================================================ softmax (thread = row of tile x)
+        const int x = warp >> 2, qd = warp & 3, r = qd * 32 + lane, j = r / T, i_tok = r - j * T;
+        const int t0 = (2 * pair + x) * T;
+        const bool present = x == 0 || hasB;
+        const bool valid = present && j < gs && t0 + i_tok < p.ntok;
+        const int nb = present ? (x == 0 ? nblkA : nblk) : 0;
+        const int pos = n0 + t0 + i_tok;
+        const float sl2 = p.scale_log2;
+        const uint32_t lane_base = tbase + ((uint32_t)(qd * 32) << 16) + x * C::kTile;
+        float m = -INFINITY, l = 0.f;
+        for (int i = 0; i < nb; ++i) {
+            mbar_wait(&s_full[x], i & 1);
+            tc_fence_after();
+            float xs[kPuBT];
+            {
+                uint32_t v0[32], v1[32];
+                tmem_ld32(lane_base, v0);
+                tmem_ld32(lane_base + 32, v1);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    xs[c] = __uint_as_float(v0[c]);
+                    xs[32 + c] = __uint_as_float(v1[c]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_free[x]);
+            float bmax = -INFINITY;
+            const int tk0 = i * kPuBT;
+#pragma unroll
+            for (int c = 0; c < kPuBT; ++c) {
+                xs[c] = (valid && tk0 + c <= pos) ? xs[c] * sl2 : -INFINITY;
+                bmax = fmaxf(bmax, xs[c]);
+            }
+            const bool raise = bmax > m + kPuRaise || (m == -INFINITY && bmax > -INFINITY);
+            const float m_new = raise ? fmaxf(m, bmax) : m;
+            const bool rescale = raise && l > 0.f;
+            if (i >= 1) {  // PV(i - 1) done: P may be overwritten and O rescaled
+                mbar_wait(&p_free[x], (i - 1) & 1);
+                tc_fence_after();
+            }
+            if (__any_sync(0xffffffffu, rescale)) {  // O holds earlier blocks
+                const float al = rescale ? ex2(m - m_new) : 1.f;
+#pragma unroll
+                for (int c0 = 0; c0 < D; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(lane_base + 128 + c0, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(__uint_as_float(v[c]) * al);
+                    tmem_st32(lane_base + 128 + c0, v);
+                }
+                tmem_wait_st();
+                l *= al;
+            }
+            m = m_new;
+            const float msafe = m == -INFINITY ? 0.f : m;
+            uint32_t hw[32], lw[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const float p0 = ex2(xs[2 * c] - msafe), p1 = ex2(xs[2 * c + 1] - msafe);
+                l += p0 + p1;
+                const __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
+                const float2 hf = __bfloat1622float2(hv);
+                hw[c] = *reinterpret_cast<const uint32_t*>(&hv);
+                lw[c] = pack_bf16(p0 - hf.x, p1 - hf.y);
+            }
+            tmem_st32(lane_base + 64, hw);
+            tmem_st32(lane_base + 96, lw);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[x]);
+        }
+        // ------------------------------------------------------------ epilogue: O / l
+        if (nb > 0) mbar_wait(&p_free[x], (nb - 1) & 1);
+        tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        float* dst = p.out + (((size_t)b * p.ntok + t0 + i_tok) * p.m + h * gs + j) * D;
+        bool bad = false;
+        if (present) {
+#pragma unroll
+            for (int c0 = 0; c0 < D; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(lane_base + 128 + c0, v);
+                tmem_wait_ld();
+                if (valid) {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 4) {
+                        const float4 o = make_float4(__uint_as_float(v[c]) * inv, __uint_as_float(v[c + 1]) * inv,
+                                                     __uint_as_float(v[c + 2]) * inv, __uint_as_float(v[c + 3]) * inv);
+                        bad |= !(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w));
+                        *reinterpret_cast<float4*>(dst + c0 + c) = o;
+                    }
+                }
+            }
+        }
+        if (valid && p.lse_out)
+            p.lse_out[((size_t)b * p.ntok + t0 + i_tok) * p.m + h * gs + j] =
+                l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
+        if (bad) set_err(p.err, kDevNumeric);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::kTmemCols));
+}
+
 }  // namespace
 
 bool prefill_umma_supported(const PrefillParams& p) { return (p.d == 128 || p.d == 64) && p.gs <= 16; }
@@ -675,6 +991,33 @@ cudaError_t launch_prefill_umma2(const PrefillParams& p, const CUtensorMap* tm_k
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((p.ntok + T - 1) / T, p.g, p.batch);
     cfg.blockDim = dim3(kPuThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    void* args[] = {const_cast<CUtensorMap*>(tm_kv), const_cast<PrefillParams*>(&p)};
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+cudaError_t launch_prefill_umma3(const PrefillParams& p, const CUtensorMap* tm_kv, cudaStream_t st, bool pdl) {
+    const void* fn = p.d == 128 ? (const void*)prefill_umma3_kernel<128> : (const void*)prefill_umma3_kernel<64>;
+    const int smem = p.d == 128 ? Pu3Cfg<128>::kSmem : Pu3Cfg<64>::kSmem;
+    static std::atomic<int> cache[kMaxDevices * 2];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+    const int slot = dev * 2 + (p.d == 128 ? 0 : 1);
+    if (cache[slot].load(std::memory_order_acquire) == 0) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        cache[slot].store(1, std::memory_order_release);
+    }
+    const int T = 128 / p.gs, ntiles = (p.ntok + T - 1) / T;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((ntiles + 1) / 2, p.g, p.batch);
+    cfg.blockDim = dim3(kPu3Threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
