@@ -659,10 +659,11 @@ prefill_umma2_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPar
 // Two query tiles per CTA on the converged-issue pipeline (pfumma = 3): tiles A = 2c and B = 2c + 1
 // of one (kv head, sequence) share every K / V block and alternate on the tensor core — S_A(i),
 // S_B(i), then PV_A(i - 1), PV_B(i - 1) — so one tile's softmax runs while the other tile's MMAs
-// execute.  TMEM budget (512 columns): per tile one S buffer (64 columns), one P buffer (hi
-// [0, 32), lo [32, 64)) and O — single-buffered per tile, the other tile fills the gaps; Q of both
-// tiles in shared memory.  (Writing P over its own S, two S/P buffers per tile, measured faster but
-// wrong: an MMA writing S over the columns the previous PV still reads is not ordered for us.)
+// execute.  TMEM budget (512 columns): per tile two 64-column S/P buffers — the softmax writes P(i)
+// (hi [0, 32), lo [32, 64)) over the S(i) it has read — and O; Q of both tiles in shared memory.
+// S_X(i) reuses the buffer of PV_X(i - 2): the MMA warp waits for that PV's completion first (an
+// MMA writing TMEM columns an earlier MMA still reads is not ordered for us: without the wait the
+// results were wrong), so the softmax never waits for the previous PV before writing its P.
 constexpr int kPu3Threads = 352;  // softmax of A: warps 0-3, of B: 4-7; K producer 8, MMA 9, V producer 10
 
 template <int D>
@@ -674,10 +675,10 @@ struct Pu3Cfg {
     static constexpr int oK = oQ + 2 * kQ;
     static constexpr int oV = oK + kPuNB * kBlk;
     static constexpr int oBar = oV + kPuNB * kBlk;
-    static constexpr int nBar = 4 * kPuNB + 1 + 4 * 2;
+    static constexpr int nBar = 4 * kPuNB + 1 + 3 * 4;
     static constexpr int kSmem = 1024 + oBar + nBar * 8 + 16;
     static constexpr int kTmemCols = 512;
-    static constexpr int kTile = 256;                            // TMEM columns per tile: S, P at +64, O at +128
+    static constexpr int kTile = 256;                            // TMEM columns per tile: S/P 2 x 64, O at +128
 };
 
 __device__ __forceinline__ void umma_ss_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -700,11 +701,10 @@ prefill_umma3_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPar
     uint64_t* v_full = k_empty + kPuNB;
     uint64_t* v_empty = v_full + kPuNB;
     uint64_t* vz_done = v_empty + kPuNB;
-    uint64_t* s_full = vz_done + 1;   // [tile]: one phase per block
-    uint64_t* s_free = s_full + 2;    // [tile]: the softmax read S
-    uint64_t* p_full = s_free + 2;    // [tile]: the softmax wrote P
-    uint64_t* p_free = p_full + 2;    // [tile]: PV completed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_free + 2);
+    uint64_t* s_full = vz_done + 1;   // [tile][buffer]: S landed
+    uint64_t* p_full = s_full + 4;    // [tile][buffer]: the softmax wrote P
+    uint64_t* p_free = p_full + 4;    // [tile][buffer]: PV completed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_free + 4);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int gs = p.gs, T = 128 / gs;
@@ -720,11 +720,10 @@ prefill_umma3_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPar
             mbar_init(&v_empty[i], 1);
         }
         mbar_init(vz_done, 1);
-        for (int x = 0; x < 2; ++x) {
-            mbar_init(&s_full[x], 1);
-            mbar_init(&s_free[x], 4);
-            mbar_init(&p_full[x], 4);
-            mbar_init(&p_free[x], 1);
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 4);
+            mbar_init(&p_free[i], 1);
         }
         fence_mbar_init();
     }
@@ -822,8 +821,8 @@ prefill_umma3_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPar
 #pragma unroll
                 for (int x = 0; x < 2; ++x) {
                     if (x == 0 ? i >= nblkA : !hasB) continue;
-                    if (i >= 1) {
-                        mbar_wait(&s_free[x], (i - 1) & 1);  // softmax_X(i - 1) read S
+                    if (i >= 2) {
+                        mbar_wait(&p_free[x * 2 + (i & 1)], ((i - 2) >> 1) & 1);  // PV_X(i - 2) left the buffer
                         tc_fence_after();
                     }
                     const uint64_t qd = q_d0 + (uint64_t)((x * C::kQ) >> 4);
@@ -831,9 +830,9 @@ prefill_umma3_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPar
                     for (int kk = 0; kk < D / 16; ++kk) {
                         const uint32_t off = (uint32_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
                         const uint32_t offk = (uint32_t)((((kk >> 2) * (kPuBT * 128)) + (kk & 3) * 32) >> 4);
-                        umma_ss_w(tb + x * C::kTile, qd + off, kd + offk, kIdS, kk > 0 ? 1u : 0u);
+                        umma_ss_w(tb + x * C::kTile + (i & 1) * 64, qd + off, kd + offk, kIdS, kk > 0 ? 1u : 0u);
                     }
-                    umma_commit_w(&s_full[x]);
+                    umma_commit_w(&s_full[x * 2 + (i & 1)]);
                 }
                 umma_commit_w(&k_empty[i % kPuNB]);
             }
@@ -846,9 +845,9 @@ prefill_umma3_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPar
 #pragma unroll
                 for (int x = 0; x < 2; ++x) {
                     if (x == 0 ? j >= nblkA : !hasB) continue;
-                    mbar_wait(&p_full[x], j & 1);
+                    mbar_wait(&p_full[x * 2 + (j & 1)], (j >> 1) & 1);
                     tc_fence_after();
-                    const uint32_t pc = tb + x * C::kTile + 64;
+                    const uint32_t pc = tb + x * C::kTile + (j & 1) * 64;
 #pragma unroll
                     for (int q = 0; q < kPuKB; ++q) {
                         if (q < np) {
@@ -857,7 +856,7 @@ prefill_umma3_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPar
                             umma_ts_w(tb + x * C::kTile + 128, pc + 32 + q * 8, bv, kIdPV, 1u);
                         }
                     }
-                    umma_commit_w(&p_free[x]);
+                    umma_commit_w(&p_free[x * 2 + (j & 1)]);
                 }
                 umma_commit_w(&v_empty[j % kPuNB]);
             }
@@ -874,13 +873,13 @@ prefill_umma3_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPar
         const uint32_t lane_base = tbase + ((uint32_t)(qd * 32) << 16) + x * C::kTile;
         float m = -INFINITY, l = 0.f;
         for (int i = 0; i < nb; ++i) {
-            mbar_wait(&s_full[x], i & 1);
+            mbar_wait(&s_full[x * 2 + (i & 1)], (i >> 1) & 1);
             tc_fence_after();
             float xs[kPuBT];
             {
                 uint32_t v0[32], v1[32];
-                tmem_ld32(lane_base, v0);
-                tmem_ld32(lane_base + 32, v1);
+                tmem_ld32(lane_base + (i & 1) * 64, v0);
+                tmem_ld32(lane_base + (i & 1) * 64 + 32, v1);
                 tmem_wait_ld();
 #pragma unroll
                 for (int c = 0; c < 32; ++c) {
@@ -888,9 +887,6 @@ prefill_umma3_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPar
                     xs[32 + c] = __uint_as_float(v1[c]);
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_free[x]);
             float bmax = -INFINITY;
             const int tk0 = i * kPuBT;
 #pragma unroll
@@ -901,11 +897,9 @@ prefill_umma3_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPar
             const bool raise = bmax > m + kPuRaise || (m == -INFINITY && bmax > -INFINITY);
             const float m_new = raise ? fmaxf(m, bmax) : m;
             const bool rescale = raise && l > 0.f;
-            if (i >= 1) {  // PV(i - 1) done: P may be overwritten and O rescaled
-                mbar_wait(&p_free[x], (i - 1) & 1);
+            if (__any_sync(0xffffffffu, rescale)) {  // O holds earlier blocks: wait for PV(i - 1)
+                mbar_wait(&p_free[x * 2 + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
                 tc_fence_after();
-            }
-            if (__any_sync(0xffffffffu, rescale)) {  // O holds earlier blocks
                 const float al = rescale ? ex2(m - m_new) : 1.f;
 #pragma unroll
                 for (int c0 = 0; c0 < D; c0 += 32) {
@@ -931,15 +925,15 @@ prefill_umma3_kernel(const __grid_constant__ CUtensorMap tm_kv, const PrefillPar
                 hw[c] = *reinterpret_cast<const uint32_t*>(&hv);
                 lw[c] = pack_bf16(p0 - hf.x, p1 - hf.y);
             }
-            tmem_st32(lane_base + 64, hw);
-            tmem_st32(lane_base + 96, lw);
+            tmem_st32(lane_base + (i & 1) * 64, hw);  // P over the S it was computed from
+            tmem_st32(lane_base + (i & 1) * 64 + 32, lw);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[x]);
+            if (lane == 0) mbar_arrive(&p_full[x * 2 + (i & 1)]);
         }
         // ------------------------------------------------------------ epilogue: O / l
-        if (nb > 0) mbar_wait(&p_free[x], (nb - 1) & 1);
+        if (nb > 0) mbar_wait(&p_free[x * 2 + ((nb - 1) & 1)], ((nb - 1) >> 1) & 1);
         tc_fence_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
         float* dst = p.out + (((size_t)b * p.ntok + t0 + i_tok) * p.m + h * gs + j) * D;
