@@ -1334,7 +1334,8 @@ const char* delta_layer_kernel_name(delta_t h, int32_t layer, int32_t batch) {
     if (!h->use_tc) return "attn_simt_kernel (fp32, cluster split-K merge)";
     if (h->tune_umma && umma_supported(p)) return "attn_umma_kernel (tcgen05, cluster split-K merge)";
     if (p.sparse_lat) return "sparse_lat_kernel (resident plan tiles, cluster DSMEM split-K merge)";
-    if (p.gmerge) return "attn_tc_kernel (one CTA per SM, global split-K merge)";
+    if (p.gmerge) return p.gll ? "attn_tc_kernel (one CTA per SM, global split-K merge over LL words)"
+                               : "attn_tc_kernel (one CTA per SM, global split-K merge)";
     return "attn_tc_kernel (cluster DSMEM split-K merge)";
 }
 
