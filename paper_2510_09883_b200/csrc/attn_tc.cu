@@ -124,8 +124,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const AttnParams p) {
     // fixed_part: the producer's first block-table entries do not depend on the length, so they
     // are loaded in the same round trip as the length counter (used if the geometry agrees)
     int spec_phys = 0;
-    const int spec_u0 = max(0, p.page_lo) +
-                        split * ((max(0, min(p.bt_stride, p.page_hi) - max(0, p.page_lo)) + p.nsplit - 1) / p.nsplit);
+    const int spec_u0 = max(0, p.page_lo) + split * fixed_pages(p);
     if (!TOKEN_PLAN && p.fixed_part && p.role != kRoleSparse && warp == NCW && lane < kBatch &&
         spec_u0 + lane < p.bt_stride)
         spec_phys = p.block_table[(size_t)b * p.bt_stride + spec_u0 + lane];

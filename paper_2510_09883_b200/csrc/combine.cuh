@@ -109,6 +109,13 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
     return (uint32_t)((c >> 3) * TileLayout<D>::kHalfBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 
+// fixed_part geometry (FULL / SELECT): pages per split of the rank's maximum range, so split c
+// starts at page lo + c * fixed_pages(p) whatever the length (split_geometry, attn_tc.cu)
+__device__ __forceinline__ int fixed_pages(const AttnParams& p) {
+    const int lo = max(0, p.page_lo), maxr = max(0, min(p.bt_stride, p.page_hi) - lo);
+    return (maxr + p.nsplit - 1) / p.nsplit;
+}
+
 // Does this rank hold logical page u (sequence sharding; always true when unsharded)?
 __device__ __forceinline__ bool owns_page(const AttnParams& p, int u) { return u >= p.page_lo && u < p.page_hi; }
 
@@ -121,7 +128,7 @@ __device__ __forceinline__ void split_geometry(const AttnParams& p, int b, int s
     if (p.role != kRoleSparse) {
         const int npages = (s + kPage - 1) / kPage;
         const int lo = max(0, p.page_lo), hi = min(npages, p.page_hi), n = max(0, hi - lo);
-        const int maxr = max(0, min(p.bt_stride, p.page_hi) - lo), pf = (maxr + p.nsplit - 1) / p.nsplit;
+        const int maxr = max(0, min(p.bt_stride, p.page_hi) - lo), pf = fixed_pages(p);
         if (p.fixed_part && n * 16 >= maxr * 15) {
             // fixed_part: split c starts at page c * ceil(max / nsplit) whatever s is (while the
             // cache is at least 15/16 full), so a producer can load its first block-table entries
