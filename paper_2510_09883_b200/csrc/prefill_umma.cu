@@ -364,12 +364,6 @@ struct Pu2Cfg {
     static constexpr int kOCol = 320;
 };
 
-__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
-}
 // Issued by the whole (converged) warp: one lane, elected inside the asm, issues the MMA — no
 // divergent `if (lane == 0)` around it, so the operands can stay in uniform registers instead
 // of the per-MMA elect / broadcast loop the compiler wraps around divergent tcgen05 issue.

@@ -171,7 +171,7 @@ __device__ __forceinline__ int topk_regs(const SelectParams& p, int n_units, int
                                       int32_t* plan, int32_t* plan_phys, uint32_t* sm_keys, int* hist2,
                                       int* scratch, uint32_t& s_and, uint32_t& s_or, int& s_bin, int& s_rem,
                                       int& s_cnt, const uint2* kll, uint32_t llf) {
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31;
     auto forced = [&](int u) { return u < sink_hi || u >= win_lo; };
     auto phys_of = [&](int u) -> int32_t { return block == 1 ? bt[u / kPage] * kPage + (u % kPage) : bt[u]; };
     // ---- register-resident path: thread t holds units [t*ipt, t*ipt + ipt) — keys,
