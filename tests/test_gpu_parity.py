@@ -549,3 +549,34 @@ def test_select_ll_keys_do_not_alias_across_delta_layers():
         for b in range(case.batch):
             for l in range(sh.L):
                 assert_close_bf16(out[l, b], ref[b][l][0], f"graph step s={s} layer {l} seq {b}")
+
+
+def test_long_graph_run_then_layer_calls_bitwise():
+    """Forty graph-replayed steps with a growing context (the LL merge and select flags cycle
+    through many launches and leave stale words behind), then the last step again through the
+    per-layer ABI from the same state: bitwise equal outputs and LSEs (same kernels, same inputs)."""
+    from paper_2510_09883_b200 import ROLE_SELECT
+    sh = Shape(L=6, m=32, g=8, d=128, F=1, delta=[1, 4], k=512, S=4, Lw=32, block=16, dtype="bf16")
+    n, s0 = 40, 8000
+    case = GpuCase(sh, 47, batch=1, s_pre=s0 - 1, max_seq=s0 + n + 16)
+    st = case.stack
+    stream = torch.cuda.Stream()
+    out = torch.empty((sh.L, 1, sh.m, sh.d), dtype=torch.float32, device="cuda")
+    lse = torch.empty((sh.L, 1, sh.m), dtype=torch.float32, device="cuda")
+    for i in range(n):
+        q, k, v = case.inputs(s0 + i)
+        stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(stream):
+            st.decode_step(q, k, v, out, lse, stream=stream)
+        stream.synchronize()
+    assert st.get_error() == 0
+    g_out, g_lse = out.clone(), lse.clone()
+    st.set_seq_lens([s0 + n - 2])
+    out2, lse2 = torch.empty_like(out), torch.empty_like(lse)
+    for l in range(sh.L):
+        st.append_decode_layer(l, k[l], v[l], q[l], out2[l], lse2[l])
+        if st.role(l) == ROLE_SELECT:
+            st.select(l, 1)
+    torch.cuda.synchronize()
+    assert st.get_error() == 0
+    assert torch.equal(g_out, out2) and torch.equal(g_lse, lse2)
